@@ -1,0 +1,194 @@
+// Device-side building blocks for the B200 log-domain Sinkhorn kernels.
+//
+// Arithmetic contract (SURVEY.md 8(a'); reference solver.py:76-115,
+// reduction.py:179-208): every potential / check / cost ARGUMENT is built with
+// separately rounded fp32 ops (__fsub_rn/__fmul_rn/__fadd_rn, never an FMA),
+// because contracting (g - C) * inv_eps + log_nu into an FFMA moves the
+// potentials by 1.3e-5 at eps=1e-4. Only what happens AFTER the
+// argument is rounded -- the shift, the exponential, the summation order -- is
+// free, and that is where the kernels get their speed (ex2.approx on the MUFU
+// pipe, fused shift+scale FFMA, warp-shuffle trees).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lsk {
+
+constexpr float kLog2e = 1.4426950408889634f;   // fl(log2 e)
+constexpr float kSumFloor = 1e-30f;             // reduction.py:44 SUM_FLOOR
+// Stale-shift sums outside [kShiftLo, kShiftHi] are recomputed exactly. With
+// ex2.approx.ftz, flushed terms are < 1.2e-38 each, so a sum >= 1e-20 is
+// exact to ~1e-13 relative even at 65536 terms.
+constexpr float kShiftLo = 1e-20f;
+constexpr float kShiftHi = 1e30f;
+
+// ---- the reference's three separately rounded ops: fl(fl(fl(a - c) * s) + l)
+__device__ __forceinline__ float arg3(float a, float c, float inv_eps, float l) {
+  return __fadd_rn(__fmul_rn(__fsub_rn(a, c), inv_eps), l);
+}
+// check argument: fl(fl(fl(fl(f + g) - c) * s) + l)   (solver.py:98-101)
+__device__ __forceinline__ float arg4(float f, float g, float c, float inv_eps, float l) {
+  return __fadd_rn(__fmul_rn(__fsub_rn(__fadd_rn(f, g), c), inv_eps), l);
+}
+
+// exp(x - shift) as 2^(x*log2e - shift*log2e): x is the exactly rounded
+// reference argument; the FFMA only re-rounds the (small) post-shift value and
+// a per-row/column constant, i.e. the SURVEY F4/F10 "free" part.
+__device__ __forceinline__ float ex2(float t) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(t));
+  return y;
+}
+__device__ __forceinline__ float exp_shifted(float x, float shift_l2e) {
+  return ex2(__fmaf_rn(x, kLog2e, -shift_l2e));
+}
+
+// NaN-propagating max, like np.maximum (reduction.py:160).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float y;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(y) : "f"(a), "f"(b));
+  return y;
+}
+
+// ---- warp reductions (xor butterfly: every lane ends with identical bits,
+// since each level adds the same two operands in swapped order).
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// (max, sum) pair merge: the online max-rescale combine.
+__device__ __forceinline__ void pair_merge(float& m, float& s, float m2, float s2) {
+  float mm = fmax_nan(m, m2);
+  float a = (m == mm) ? 1.f : ex2((m - mm) * kLog2e);
+  float b = (m2 == mm) ? 1.f : ex2((m2 - mm) * kLog2e);
+  if (!(mm > -INFINITY)) { a = 1.f; b = 1.f; }   // both empty / NaN: keep sums
+  s = s * a + s2 * b;
+  m = mm;
+}
+__device__ __forceinline__ void warp_pair(float& m, float& s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    pair_merge(m, s, m2, s2);
+  }
+}
+
+// Block-wide sum/max of K values per thread, one __syncthreads. `red` holds
+// K * 32 floats. Every thread returns the identical result.
+template <int NT, int K, bool MAX>
+__device__ __forceinline__ void block_reduce(float (&v)[K], float* red) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k] = MAX ? warp_max(v[k]) : warp_sum(v[k]);
+    if (lane == 0) red[k * 32 + w] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    float t = lane < NW ? red[k * 32 + lane] : (MAX ? -INFINITY : 0.f);
+    v[k] = MAX ? warp_max(t) : warp_sum(t);
+  }
+}
+
+// Block-wide (max, sum) pair reduction, one __syncthreads; `red` holds 64*K.
+template <int NT, int K>
+__device__ __forceinline__ void block_pair(float (&m)[K], float (&s)[K], float* red) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    warp_pair(m[k], s[k]);
+    if (lane == 0) { red[k * 64 + w] = m[k]; red[k * 64 + 32 + w] = s[k]; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    float mm = lane < NW ? red[k * 64 + lane] : -INFINITY;
+    float ss = lane < NW ? red[k * 64 + 32 + lane] : 0.f;
+    warp_pair(mm, ss);
+    m[k] = mm; s[k] = ss;
+  }
+}
+
+// LSE finalisation exactly as reduction.py:196-207 given the shift M and the
+// shifted sum S: non-finite M (an all -inf / NaN row) yields -inf.
+__device__ __forceinline__ float lse_finish(float M, float S) {
+  if (!(fabsf(M) <= 3.402823466e38f)) return -INFINITY;
+  return __fadd_rn(M, logf(fmaxf(S, kSumFloor)));
+}
+
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) + mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---- L2-coherent loads for data produced by other CTAs of the same launch.
+__device__ __forceinline__ float ldcg(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ float4 ldcg4(const float4* p) { return __ldcg(p); }
+
+// ---- software grid barrier for the persistent (cooperatively launched)
+// solver: a monotonic arrival counter, so no reset race; target = (#barriers
+// passed so far) * gridDim.x.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch) {
+  __syncthreads();
+  epoch += 1;
+  if (threadIdx.x == 0) {
+    const unsigned target = epoch * gridDim.x;
+    __threadfence();
+    atomicAdd(counter, 1u);
+    while (ld_acquire(counter) < target) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace lsk
