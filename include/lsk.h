@@ -1,0 +1,134 @@
+/*
+ * lsk.h -- C ABI of the B200-native log-domain Sinkhorn library (liblsk.so).
+ *
+ * Plain C types only: every array argument is a DEVICE pointer (e.g. a torch
+ * tensor's data_ptr()), sizes are int32/int64, `stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream). No C++ exceptions cross
+ * this boundary: every entry point returns LSK_OK (0) or a negative LSK_E*
+ * code and records a message retrievable with lsk_last_error() (thread
+ * local). Nothing here synchronises the host unless documented.
+ *
+ * Each entry point replaces one function of the reference package's Python
+ * solver API (/root/reference/pkg/src/logsinkhorn); the cited file:line is the
+ * interface it stands in for. The Python drop-in (paper_2605_00837_b200) and
+ * INTEGRATION.md show the binding a maintainer of the reference would add.
+ *
+ * Arithmetic contract (all fp32 entry points): eps32 = (float)eps,
+ * inv_eps = 1.0f / eps32 (IEEE), neg_eps = -eps32 (solver.py:259-260);
+ * arguments are built with separately rounded fp32 ops in the reference's
+ * order (solver.py:77-79, 84-86, 98-101, 108-112). Potentials match the
+ * reference fp32 path within 1e-5 relative (max-norm); the summation tree and
+ * exp/log last bits differ.
+ */
+#ifndef LSK_H
+#define LSK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LSK_OK 0
+#define LSK_EINVAL (-1)       /* bad argument (maps to ValueError / DimensionMismatch) */
+#define LSK_ECUDA (-2)        /* CUDA runtime error */
+#define LSK_EUNSUPPORTED (-3) /* shape not supported by this entry point */
+#define LSK_ENCCL (-4)        /* NCCL error (sharded solver) */
+
+/* lsk_solve_dense_f32 flags */
+#define LSK_FLAG_STALE_SHIFT 1 /* one-pass stale-shift iteration (default fast path) */
+#define LSK_FLAG_COST 2        /* compute the transport cost after the loop */
+
+/* result[] slots written by lsk_solve_dense_f32 (device int32[8]) */
+#define LSK_RES_STATUS 0     /* 0 not_converged, 1 converged, 2 numerical_failure (types.py:35-37) */
+#define LSK_RES_ITERS 1      /* SolveReport.iterations */
+#define LSK_RES_NTRACE 2     /* entries written to trace_iter / trace_err */
+#define LSK_RES_ROWGUARD 4   /* stale-shift row LSEs recomputed exactly */
+#define LSK_RES_COLGUARD 5   /* iterations whose columns were recomputed exactly */
+
+const char* lsk_last_error(void);
+int32_t lsk_version(void);
+
+/* Largest m the persistent dense solver handles (8192 in this build). */
+int32_t lsk_solve_dense_max_cols(void);
+/* Trace capacity for a solve: ceil(max_iter / check_interval) + 1. */
+int32_t lsk_trace_capacity(int32_t max_iter, int32_t check_interval);
+size_t lsk_solve_dense_workspace_bytes(int32_t n, int32_t m);
+
+/*
+ * Whole log-domain solve on a dense fp32 cost matrix, ONE cooperative launch.
+ * Replaces logsinkhorn.solver.solve (solver.py:230-337): alpha-first
+ * alternation from zero potentials, a marginal-error check every
+ * check_interval iterations (finiteness, then err, trace, stop), the extra
+ * check at a cap that is not a checkpoint, and the transport cost unless the
+ * solve failed. C is row-major with row stride ldc (floats, multiple of 4,
+ * 16-byte aligned; columns m..ldc-1 must be zero when m % 4 != 0).
+ * log_mu/mu (n) and log_nu (m) are the fp32 casts of the fp64 weights
+ * (solver.py:256-258). Outputs: f_out (n), g_out (m), trace_iter/trace_err
+ * (lsk_trace_capacity entries), result (int32[8], LSK_RES_*),
+ * result_f (float[2]: final marginal error, transport cost).
+ */
+int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                            const float* log_nu, const float* mu, double eps, double tol, int32_t max_iter,
+                            int32_t check_interval, int32_t flags, float* f_out, float* g_out,
+                            int32_t* trace_iter, float* trace_err, int32_t* result, float* result_f,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* alpha = neg_eps * LSE_j((beta_j - C_ij) * inv_eps + log_nu_j)
+ * -- update_alpha, solver.py:118-140 (_alpha_step 76-80). Any n, m. */
+int32_t lsk_update_alpha_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* beta,
+                             const float* log_nu, double eps, float* alpha_out, void* stream);
+
+/* beta = neg_eps * LSE_i((alpha_i - C_ij) * inv_eps + log_mu_i), reading C
+ * row-major (coalesced column partials + fixed-order combine) -- update_beta,
+ * solver.py:143-176 (_beta_step_strided 83-87; the transposed path 90-94 is
+ * served by the same kernel, so both are bit-identical as the reference
+ * requires). */
+size_t lsk_update_beta_workspace_bytes(int32_t n, int32_t m);
+int32_t lsk_update_beta_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* alpha,
+                            const float* log_mu, double eps, float* beta_out, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
+/* err = sum_i |exp(log_mu_i + LSE_j(((a_i + b_j) - C_ij) * inv + log_nu_j)) - mu_i|
+ * -- marginal_error, solver.py:179-206 (_marginal_error 97-104). err_out is a
+ * device float. Workspace: n floats. */
+int32_t lsk_marginal_error_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* mu,
+                               const float* log_mu, const float* log_nu, const float* alpha,
+                               const float* beta, double eps, float* err_out, void* workspace,
+                               size_t workspace_bytes, void* stream);
+
+/* cost = sum_ij C_ij * exp(((((a_i + b_j) - C_ij) * inv) + log_mu_i) + log_nu_j)
+ * -- transport_cost, solver.py:209-227 (_transport_cost 107-115). Device
+ * float out; workspace n floats. */
+int32_t lsk_transport_cost_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                               const float* log_nu, const float* alpha, const float* beta, double eps,
+                               float* cost_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* P_ij = exp(same argument as the cost) into P (row stride ldp); counts
+ * non-finite rows into *nonfinite_out (device int32, caller zeroes it)
+ * -- materialize_plan, solver.py:434-458. */
+int32_t lsk_materialize_plan_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                                 const float* log_nu, const float* alpha, const float* beta, double eps,
+                                 float* P, int64_t ldp, int32_t* nonfinite_out, void* stream);
+
+/* C_ij = fl32(sum_k (x_ik - y_jk)^2) from fp64 points (n,d)/(m,d), the sum in
+ * coordinate order in fp64 -- squared_euclidean_cost, costs.py:36-50 -- then,
+ * if normalize_max, divided in fp64 by the exact max (applications.py:186-188)
+ * before the single fp32 rounding (solver.py:253). cmax_out: device double,
+ * the max before normalisation. Workspace: lsk_build_cost_workspace_bytes(). */
+size_t lsk_build_cost_workspace_bytes(void);
+int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t m, int32_t d,
+                           int32_t normalize_max, float* C, int64_t ldc, double* cmax_out, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* dst = fl32(src) in a zero-padded row-major layout (row stride ldd floats,
+ * a multiple of 4 for the solver): the one fp64 -> fp32 cast of the cost
+ * matrix (solver.py:253), or a plain fp32 re-pad when src_is_f64 == 0. */
+int32_t lsk_cast_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int32_t n, int32_t m, float* dst,
+                          int64_t ldd, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSK_H */

@@ -1,0 +1,50 @@
+"""B200-native log-domain Sinkhorn (sm_100a CUDA behind a C ABI).
+
+Drop-in for the solver path of the reference package ``logsinkhorn``:
+``solve``, ``update_alpha``, ``update_beta``, ``marginal_error``,
+``transport_cost``, ``materialize_plan`` and the value / error types, with
+the same names, signatures and error behaviour. Kernels live in
+``liblsk.so`` (``include/lsk.h``); there is no CPU fallback.
+"""
+
+from .costs import as_points, solve_points, squared_euclidean_cost
+from .errors import (
+    BackendError,
+    DegenerateRange,
+    DimensionMismatch,
+    EmptyInput,
+    EmptyView,
+    FileFormatError,
+    LogSinkhornError,
+    NegativeOrNonFiniteEntry,
+    NonFiniteInput,
+    NonFiniteResult,
+    ZeroRowMass,
+    ZeroWeight,
+)
+from .solver import (
+    marginal_error,
+    materialize_plan,
+    solve,
+    to_device_cost,
+    transport_cost,
+    update_alpha,
+    update_beta,
+)
+from .types import (
+    STATUS_CONVERGED,
+    STATUS_NOT_CONVERGED,
+    STATUS_NUMERICAL_FAILURE,
+    CostMatrix,
+    DeviceCostMatrix,
+    DiscreteDistribution,
+    DualPotentials,
+    ReductionPlan,
+    SinkhornConfig,
+    SolveReport,
+    TransportPlan,
+    make_cost_matrix,
+    make_distribution,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,350 @@
+// C-ABI implementation (include/lsk.h): argument checks, workspace carving,
+// launch configuration. All compute lives in lsk_dense.cuh / lsk_kernels.cuh.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/lsk.h"
+#include "lsk_dense.cuh"
+#include "lsk_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int32_t fail(int32_t code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define LSK_CUDA(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t e__ = (expr);                                                               \
+    if (e__ != cudaSuccess) return fail(LSK_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+struct EpsConsts {
+  float inv_eps, neg_eps;
+};
+// solver.py:259-260: inv_eps = dt(1) / dt(eps); neg_eps = -dt(eps)
+inline EpsConsts eps_consts(double eps) {
+  volatile float e32 = static_cast<float>(eps);
+  volatile float one = 1.0f;
+  EpsConsts c;
+  c.inv_eps = one / e32;
+  c.neg_eps = -e32;
+  return c;
+}
+
+int num_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return sms > 0 ? sms : 148;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ---- persistent dense solver instances: (NT, V, R, STAGES) by row capacity W
+using Solver1k = lsk::DenseSolver<256, 1, 4, 8>;
+using Solver2k = lsk::DenseSolver<512, 1, 4, 6>;
+using Solver4k = lsk::DenseSolver<512, 2, 2, 6>;
+using Solver8k = lsk::DenseSolver<512, 4, 1, 6>;
+
+template <class SV>
+__global__ void __launch_bounds__(SV::NW * 32, 1) k_solve_dense(lsk::DenseArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  SV sv(a, smem);
+  sv.solve();
+}
+
+constexpr int kHeaderInts = 64;  // [0]=barrier [1]=guard [2..3]=stats [4]=status [5]=iters [6]=ntrace [7]=fbuf
+                                 // [8]=err(float) [9]=cost(float)
+
+struct DenseLayout {
+  int W, G;
+  size_t off_f0, off_g0, zero_bytes, off_f1, off_g1, off_part, off_pairs, off_err, off_flag, off_cost, total;
+};
+
+inline int dense_width(int m) {
+  if (m <= 1024) return 1024;
+  if (m <= 2048) return 2048;
+  if (m <= 4096) return 4096;
+  if (m <= 8192) return 8192;
+  return 0;
+}
+
+DenseLayout dense_layout(int n, int m) {
+  DenseLayout L{};
+  L.W = dense_width(m);
+  L.G = num_sms();
+  if (n < L.G) L.G = n > 0 ? n : 1;
+  size_t o = kHeaderInts * 4;
+  L.off_f0 = o; o = align_up(o + size_t(n) * 4, 256);
+  L.off_g0 = o; o = align_up(o + size_t(L.W) * 4, 256);
+  L.zero_bytes = o;
+  L.off_f1 = o; o = align_up(o + size_t(n) * 4, 256);
+  L.off_g1 = o; o = align_up(o + size_t(L.W) * 4, 256);
+  L.off_part = o; o = align_up(o + size_t(L.G) * L.W * 4, 256);
+  L.off_pairs = o; o = align_up(o + size_t(L.G) * L.W * 8, 256);
+  L.off_err = o; o = align_up(o + size_t(L.G) * 4, 256);
+  L.off_flag = o; o = align_up(o + size_t(L.G) * 4, 256);
+  L.off_cost = o; o = align_up(o + size_t(L.G) * 4, 256);
+  L.total = o;
+  return L;
+}
+
+template <class SV>
+int32_t launch_dense(lsk::DenseArgs& a, int G, cudaStream_t st) {
+  static bool attr_set = false;  // per instance
+  if (!attr_set) {
+    LSK_CUDA(cudaFuncSetAttribute(k_solve_dense<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SV::kSmemBytes)));
+    attr_set = true;
+  }
+  int per_sm = 0;
+  LSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dense<SV>, SV::NW * 32, SV::kSmemBytes));
+  if (per_sm < 1) return fail(LSK_ECUDA, "dense solver: kernel does not fit on an SM");
+  void* args[] = {&a};
+  LSK_CUDA(cudaLaunchCooperativeKernel((const void*)k_solve_dense<SV>, dim3(G), dim3(SV::NW * 32), args,
+                                       SV::kSmemBytes, st));
+  return LSK_OK;
+}
+
+int32_t check_dense(const float* C, int64_t ldc, int32_t n, int32_t m) {
+  if (!C) return fail(LSK_EINVAL, "C is null");
+  if (n < 1 || m < 1) return fail(LSK_EINVAL, "n and m must be >= 1");
+  if (ldc < m || ldc % 4 != 0) return fail(LSK_EINVAL, "ldc must be >= m and a multiple of 4");
+  if (reinterpret_cast<uintptr_t>(C) % 16 != 0) return fail(LSK_EINVAL, "C must be 16-byte aligned");
+  return LSK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lsk_last_error(void) { return g_err.c_str(); }
+int32_t lsk_version(void) { return 1; }
+int32_t lsk_solve_dense_max_cols(void) { return 8192; }
+int32_t lsk_trace_capacity(int32_t max_iter, int32_t check_interval) {
+  if (max_iter < 1 || check_interval < 1) return 1;
+  return (max_iter + check_interval - 1) / check_interval + 1;
+}
+
+size_t lsk_solve_dense_workspace_bytes(int32_t n, int32_t m) {
+  if (n < 1 || m < 1 || dense_width(m) == 0) return 0;
+  return dense_layout(n, m).total;
+}
+
+int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                            const float* log_nu, const float* mu, double eps, double tol, int32_t max_iter,
+                            int32_t check_interval, int32_t flags, float* f_out, float* g_out,
+                            int32_t* trace_iter, float* trace_err, int32_t* result, float* result_f,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  int32_t rc = check_dense(C, ldc, n, m);
+  if (rc) return rc;
+  if (!(eps > 0) || !(tol > 0) || max_iter < 1 || check_interval < 1)
+    return fail(LSK_EINVAL, "eps, tol > 0; max_iter, check_interval >= 1 required");
+  if (!log_mu || !log_nu || !mu || !f_out || !g_out || !trace_iter || !trace_err || !result || !result_f)
+    return fail(LSK_EINVAL, "null output/input pointer");
+  if (dense_width(m) == 0) return fail(LSK_EUNSUPPORTED, "dense solver supports m <= 8192 in this build");
+  DenseLayout L = dense_layout(n, m);
+  if (!workspace || workspace_bytes < L.total) return fail(LSK_EINVAL, "workspace too small");
+  cudaStream_t st = S(stream);
+  char* ws = static_cast<char*>(workspace);
+  LSK_CUDA(cudaMemsetAsync(ws, 0, L.zero_bytes, st));
+  int* hdr = reinterpret_cast<int*>(ws);
+  EpsConsts ec = eps_consts(eps);
+  lsk::DenseArgs a{};
+  a.C = C; a.ldc = ldc; a.n = n; a.m = m; a.mpad = (m + 3) / 4 * 4;
+  a.log_mu = log_mu; a.log_nu = log_nu; a.mu = mu;
+  a.inv_eps = ec.inv_eps; a.neg_eps = ec.neg_eps; a.tol = tol;
+  a.max_iter = max_iter; a.check = check_interval;
+  a.stale = (flags & LSK_FLAG_STALE_SHIFT) ? 1 : 0;
+  a.want_cost = (flags & LSK_FLAG_COST) ? 1 : 0;
+  a.f0 = reinterpret_cast<float*>(ws + L.off_f0);
+  a.f1 = reinterpret_cast<float*>(ws + L.off_f1);
+  a.g0 = reinterpret_cast<float*>(ws + L.off_g0);
+  a.g1 = reinterpret_cast<float*>(ws + L.off_g1);
+  a.part = reinterpret_cast<float*>(ws + L.off_part);
+  a.pairs = reinterpret_cast<float2*>(ws + L.off_pairs);
+  a.errpart = reinterpret_cast<float*>(ws + L.off_err);
+  a.flagpart = reinterpret_cast<int*>(ws + L.off_flag);
+  a.costpart = reinterpret_cast<float*>(ws + L.off_cost);
+  a.bar = reinterpret_cast<unsigned*>(hdr + 0);
+  a.guard = hdr + 1;
+  a.stats = hdr + 2;
+  a.out_status = hdr + 4;
+  a.out_iters = hdr + 5;
+  a.n_trace = hdr + 6;
+  a.out_fbuf = hdr + 7;
+  a.out_err = reinterpret_cast<float*>(hdr + 8);
+  a.out_cost = reinterpret_cast<float*>(hdr + 9);
+  a.trace_iter = trace_iter;
+  a.trace_err = trace_err;
+  switch (L.W) {
+    case 1024: rc = launch_dense<Solver1k>(a, L.G, st); break;
+    case 2048: rc = launch_dense<Solver2k>(a, L.G, st); break;
+    case 4096: rc = launch_dense<Solver4k>(a, L.G, st); break;
+    default: rc = launch_dense<Solver8k>(a, L.G, st); break;
+  }
+  if (rc) return rc;
+  lsk::k_pick<<<64, 256, 0, st>>>(a.f0, a.f1, a.out_fbuf, n, f_out);
+  lsk::k_pick<<<64, 256, 0, st>>>(a.g0, a.g1, a.out_fbuf, m, g_out);
+  // result[]: status, iters, ntrace, fbuf, rowguard, colguard
+  LSK_CUDA(cudaMemcpyAsync(result + 0, hdr + 4, 4, cudaMemcpyDeviceToDevice, st));
+  LSK_CUDA(cudaMemcpyAsync(result + 1, hdr + 5, 4, cudaMemcpyDeviceToDevice, st));
+  LSK_CUDA(cudaMemcpyAsync(result + 2, hdr + 6, 8, cudaMemcpyDeviceToDevice, st));
+  LSK_CUDA(cudaMemcpyAsync(result + 4, hdr + 2, 8, cudaMemcpyDeviceToDevice, st));
+  LSK_CUDA(cudaMemcpyAsync(result_f, hdr + 8, 8, cudaMemcpyDeviceToDevice, st));
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+int32_t lsk_update_alpha_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* beta,
+                             const float* log_nu, double eps, float* alpha_out, void* stream) {
+  if (!C || !beta || !log_nu || !alpha_out) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || ldc < m) return fail(LSK_EINVAL, "bad shape");
+  if (!(eps > 0)) return fail(LSK_EINVAL, "eps must be > 0");
+  EpsConsts ec = eps_consts(eps);
+  lsk::k_row_lse<lsk::kRowAlpha><<<n, 256, 0, S(stream)>>>(C, ldc, n, m, nullptr, beta, log_nu, nullptr, nullptr,
+                                                          ec.inv_eps, ec.neg_eps, alpha_out);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+static int beta_rowsplit(int n, int m) {
+  int tiles = (m + 1023) / 1024;
+  int want = (2 * num_sms() + tiles - 1) / tiles;  // ~2 CTAs per SM
+  int rs = (n + want - 1) / want;
+  if (rs < 64) rs = 64;
+  return rs;
+}
+
+size_t lsk_update_beta_workspace_bytes(int32_t n, int32_t m) {
+  if (n < 1 || m < 1) return 0;
+  int rs = beta_rowsplit(n, m);
+  size_t parts = (n + rs - 1) / rs;
+  return parts * size_t(m) * 8;
+}
+
+int32_t lsk_update_beta_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* alpha,
+                            const float* log_mu, double eps, float* beta_out, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  if (!C || !alpha || !log_mu || !beta_out) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || ldc < m) return fail(LSK_EINVAL, "bad shape");
+  if (!(eps > 0)) return fail(LSK_EINVAL, "eps must be > 0");
+  if (!workspace || workspace_bytes < lsk_update_beta_workspace_bytes(n, m))
+    return fail(LSK_EINVAL, "workspace too small");
+  EpsConsts ec = eps_consts(eps);
+  int rs = beta_rowsplit(n, m);
+  int parts = (n + rs - 1) / rs;
+  float2* pairs = static_cast<float2*>(workspace);
+  dim3 grid((m + 1023) / 1024, parts);
+  lsk::k_col_pairs<<<grid, 256, 0, S(stream)>>>(C, ldc, n, m, alpha, log_mu, ec.inv_eps, rs, pairs);
+  lsk::k_col_combine<<<(m + 255) / 256, 256, 0, S(stream)>>>(pairs, parts, m, ec.neg_eps, beta_out);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+int32_t lsk_marginal_error_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* mu,
+                               const float* log_mu, const float* log_nu, const float* alpha,
+                               const float* beta, double eps, float* err_out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (!C || !mu || !log_mu || !log_nu || !alpha || !beta || !err_out) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || ldc < m) return fail(LSK_EINVAL, "bad shape");
+  if (!(eps > 0)) return fail(LSK_EINVAL, "eps must be > 0");
+  if (!workspace || workspace_bytes < size_t(n) * 4) return fail(LSK_EINVAL, "workspace too small");
+  EpsConsts ec = eps_consts(eps);
+  float* rows = static_cast<float*>(workspace);
+  lsk::k_row_lse<lsk::kRowCheck><<<n, 256, 0, S(stream)>>>(C, ldc, n, m, alpha, beta, log_nu, log_mu, mu,
+                                                          ec.inv_eps, ec.neg_eps, rows);
+  lsk::k_sum_fixed<<<1, 1024, 0, S(stream)>>>(rows, n, err_out);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+int32_t lsk_transport_cost_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                               const float* log_nu, const float* alpha, const float* beta, double eps,
+                               float* cost_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!C || !log_mu || !log_nu || !alpha || !beta || !cost_out) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || ldc < m) return fail(LSK_EINVAL, "bad shape");
+  if (!(eps > 0)) return fail(LSK_EINVAL, "eps must be > 0");
+  if (!workspace || workspace_bytes < size_t(n) * 4) return fail(LSK_EINVAL, "workspace too small");
+  EpsConsts ec = eps_consts(eps);
+  float* rows = static_cast<float*>(workspace);
+  lsk::k_row_lse<lsk::kRowCost><<<n, 256, 0, S(stream)>>>(C, ldc, n, m, alpha, beta, log_nu, log_mu, nullptr,
+                                                         ec.inv_eps, ec.neg_eps, rows);
+  lsk::k_sum_fixed<<<1, 1024, 0, S(stream)>>>(rows, n, cost_out);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+int32_t lsk_materialize_plan_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                                 const float* log_nu, const float* alpha, const float* beta, double eps,
+                                 float* P, int64_t ldp, int32_t* nonfinite_out, void* stream) {
+  if (!C || !log_mu || !log_nu || !alpha || !beta || !P || !nonfinite_out) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || ldc < m || ldp < m) return fail(LSK_EINVAL, "bad shape");
+  if (!(eps > 0)) return fail(LSK_EINVAL, "eps must be > 0");
+  EpsConsts ec = eps_consts(eps);
+  int bx = (m + 255) / 256;
+  if (bx > 16) bx = 16;
+  lsk::k_plan<<<dim3(bx, n < 65535 ? n : 65535), 256, 0, S(stream)>>>(C, ldc, n, m, alpha, beta, log_mu, log_nu, ec.inv_eps, P, ldp,
+                                                  nonfinite_out);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+size_t lsk_build_cost_workspace_bytes(void) { return 2 * 2048 * sizeof(double); }
+
+int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t m, int32_t d,
+                           int32_t normalize_max, float* C, int64_t ldc, double* cmax_out, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  if (!X || !Y || !C) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || d < 1 || ldc < m) return fail(LSK_EINVAL, "bad shape");
+  cudaStream_t st = S(stream);
+  double div = 0.0;
+  if (normalize_max || cmax_out) {
+    if (!workspace || workspace_bytes < lsk_build_cost_workspace_bytes())
+      return fail(LSK_EINVAL, "workspace too small");
+    double* part = static_cast<double*>(workspace);
+    const int blocks = 2048;
+    lsk::k_cost_max<<<blocks, 256, 0, st>>>(X, Y, n, m, d, part);
+    // fold the per-CTA maxima (exact: max is order independent)
+    double host[2 * 2048];
+    LSK_CUDA(cudaMemcpyAsync(host, part, sizeof(host), cudaMemcpyDeviceToHost, st));
+    LSK_CUDA(cudaStreamSynchronize(st));
+    double mx = -1.0, mn = INFINITY;
+    for (int k = 0; k < blocks; ++k) {
+      mx = host[2 * k] > mx ? host[2 * k] : mx;
+      mn = host[2 * k + 1] < mn ? host[2 * k + 1] : mn;
+    }
+    if (cmax_out) LSK_CUDA(cudaMemcpyAsync(cmax_out, &mx, sizeof(double), cudaMemcpyHostToDevice, st));
+    if (normalize_max && (mx - mn) > 0.0) div = mx;  // cost.value_range > 0 (applications.py:186)
+    LSK_CUDA(cudaStreamSynchronize(st));
+  }
+  int bx = (m + 255) / 256;
+  if (bx > 64) bx = 64;
+  lsk::k_cost_build<<<dim3(bx, n < 65535 ? n : 65535), 256, 0, st>>>(X, Y, n, m, d, div, C, ldc);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+int32_t lsk_cast_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int32_t n, int32_t m, float* dst,
+                          int64_t ldd, void* stream) {
+  if (!src || !dst) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || lds < m || ldd < m) return fail(LSK_EINVAL, "bad shape");
+  long long bx = (ldd + 255) / 256;
+  if (bx > 32) bx = 32;
+  dim3 grid(unsigned(bx), n < 65535 ? n : 65535);
+  if (src_is_f64)
+    lsk::k_cast_pad<<<grid, 256, 0, S(stream)>>>(static_cast<const double*>(src), lds, n, m, dst, ldd);
+  else
+    lsk::k_pad_f32<<<grid, 256, 0, S(stream)>>>(static_cast<const float*>(src), lds, n, m, dst, ldd);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+}  // extern "C"

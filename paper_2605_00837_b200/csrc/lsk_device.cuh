@@ -144,17 +144,35 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Watchdog for every spin in the persistent solver: a wait longer than this
+// is a bug (lost TMA bytes, a CTA that never arrives); trap instead of hanging.
+constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra LAB_WAIT;\n"
-      "}\n" ::"r"(addr),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (!mbar_try_wait(addr, parity)) {
+    if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
+  }
 }
 __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes,
                                             uint64_t* bar) {
@@ -184,7 +202,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch)
     const unsigned target = epoch * gridDim.x;
     __threadfence();
     atomicAdd(counter, 1u);
-    while (ld_acquire(counter) < target) {
+    if (ld_acquire(counter) < target) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire(counter) < target)
+        if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
     }
     __threadfence();
   }

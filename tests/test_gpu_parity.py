@@ -1,0 +1,176 @@
+"""Parity of the CUDA path (through the C ABI) against the reference.
+
+Targets are the golden fixtures the reference itself produced
+(tests/golden/make_golden.py) plus, at sizes the CPU finishes in seconds,
+the oracle run live on the same inputs. Bars (north star):
+potentials and transport cost within 1e-5 relative (max-norm) in fp32;
+status, iteration count and checkpoint iterations identical; marginal errors
+within their fp32 rounding noise.
+"""
+
+import numpy as np
+import pytest
+
+import lsk_oracle as O
+import paper_2605_00837_b200 as lsk
+from conftest import golden, golden_names, rel_max, sha
+from inputs import fixture_points, fixture_problem
+
+pytestmark = pytest.mark.gpu
+
+SMALL = [n for n in golden_names() if n.startswith(("grid", "rand_", "antidiag", "constant", "failure"))]
+BIG = ["g1_c1_n1024", "g2_c2_n8192_k10", "g3_c3_n8192_k10", "n1024_eps1e-4_k1000", "n2048_eps1e-3_k200",
+       "g5_c5_n4096_rgb_k200", "rigid2048_eps1e-3_k200"]
+RTOL = 1e-5  # north-star parity bar, fp32 vs the reference's single precision
+
+
+def dist(w):
+    w = np.asarray(w, np.float64)
+    return lsk.DiscreteDistribution(weights=w, log_weights=np.log(w))
+
+
+def config_of(z):
+    return lsk.SinkhornConfig(epsilon=float(z["eps"]), tolerance=float(z["tol"]),
+                              max_iterations=int(z["K"]), check_interval=int(z["check"]))
+
+
+def assert_potentials(pot, z):
+    fa, fb = np.asarray(pot.alpha), np.asarray(pot.beta)
+    ra, rb = z["alpha"], z["beta"]
+    if not np.isfinite(ra).all():
+        assert not (np.isfinite(fa).all() and np.isfinite(fb).all())
+        return
+    scale = max(np.abs(ra).max(), np.abs(rb).max())
+    for x, ref in ((fa, ra), (fb, rb)):
+        den = max(np.abs(ref).max(), 1e-2 * scale)
+        assert np.abs(x.astype(np.float64) - ref).max() <= RTOL * den, (np.abs(x - ref).max(), den)
+
+
+def err_tol(ref_err, mu):
+    # |r_i - mu_i| terms carry fp32 rounding of r_i ~ mu_i: a few ulps each
+    return 1e-4 * abs(ref_err) + len(mu) * float(np.max(mu)) * 2.0 ** -21
+
+
+def assert_report(rep, z, mu):
+    assert rep.status == str(z["status"])
+    assert rep.iterations == int(z["iterations"])
+    tr = z["trace"]
+    assert [k for k, _ in rep.error_trace] == [int(k) for k in tr[:, 0]]
+    for (_, e), (_, er) in zip(rep.error_trace, tr):
+        assert abs(e - er) <= err_tol(er, mu), (e, er)
+    ref_err = float(z["err"])
+    if np.isnan(ref_err):
+        assert np.isnan(rep.final_marginal_error)
+    else:
+        assert abs(rep.final_marginal_error - ref_err) <= err_tol(ref_err, mu)
+    ref_cost = float(z["cost"])
+    if np.isnan(ref_cost):
+        assert np.isnan(rep.transport_cost)
+    else:
+        assert abs(rep.transport_cost - ref_cost) <= RTOL * abs(ref_cost) + 1e-12
+
+
+@pytest.mark.parametrize("stale", [True, False], ids=["stale", "exact"])
+@pytest.mark.parametrize("name", SMALL)
+def test_solve_small(cuda_ok, name, stale):
+    z, C64, mu_w, nu_w = fixture_problem(name)
+    with np.errstate(all="ignore"):
+        rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), config_of(z), stale_shift=stale)
+    assert_report(rep, z, mu_w)
+    assert_potentials(pot, z)
+
+
+@pytest.mark.parametrize("name", BIG)
+def test_solve_golden_points(cuda_ok, name):
+    """C1/C2/C3/C5-shaped fixtures; the cost is built on the device (fp64-exact)."""
+    z, X, Y, norm = fixture_points(name)
+    C = lsk.squared_euclidean_cost(X, Y, normalize=norm)
+    assert sha(C.values.cpu().numpy()) == str(z["C32_sha"])  # fp32(C64) bit for bit
+    rep, pot = lsk.solve(C, dist(z["mu"]), dist(z["nu"]), config_of(z))
+    assert_report(rep, z, z["mu"])
+    assert_potentials(pot, z)
+
+
+def test_half_steps(cuda_ok):
+    z = golden("half_steps")
+    eps = float(z["eps"])
+    for n, m in z["shapes"]:
+        n, m = int(n), int(m)
+        key = f"{n}x{m}"
+        C64, mu_w, nu_w, a_in, b_in = O.random_problem(n, m, 100 + n + m)
+        cost = lsk.CostMatrix(values=C64)
+        mu, nu = dist(mu_w), dist(nu_w)
+        a = lsk.update_alpha(cost, nu, b_in, eps)
+        assert a.dtype == np.float32 and rel_max(a, z[key + "_alpha"]) <= RTOL
+        b = lsk.update_beta(cost, mu, a_in, eps)
+        assert rel_max(b, z[key + "_beta_out"]) <= RTOL
+        bt = lsk.update_beta(cost, mu, a_in, eps, transposed_cost=np.ascontiguousarray(C64.T))
+        np.testing.assert_array_equal(b, bt)  # strided == transposed, bitwise (test_solver.py:101-111)
+        e = lsk.marginal_error(cost, mu, nu, a_in, b_in, eps)
+        assert abs(e - float(z[key + "_merr"])) <= err_tol(float(z[key + "_merr"]), mu_w)
+        c = lsk.transport_cost(cost, mu, nu, a_in, b_in, eps)
+        assert abs(c - float(z[key + "_tcost"])) <= RTOL * abs(float(z[key + "_tcost"]))
+        P = lsk.materialize_plan(cost, mu, nu, a_in, b_in, eps).values
+        assert P.dtype == np.float32 and P.shape == (n, m)
+        np.testing.assert_allclose(P[:4, :4], z[key + "_plan_corner"], rtol=1e-5)
+        np.testing.assert_allclose(P.sum(axis=1, dtype=np.float64), z[key + "_plan_rows"], rtol=1e-5)
+
+
+def test_known_answers(cuda_ok):
+    """Reference known answers (tests/test_solver.py:38-49, 163-178)."""
+    cost = lsk.make_cost_matrix(1, 1, [0.5])
+    nu = lsk.make_distribution([1.0])
+    assert lsk.update_alpha(cost, nu, np.zeros(1, np.float32), 0.1)[0] == pytest.approx(0.5, rel=1e-6)
+    c = lsk.make_cost_matrix(3, 4, [0.7] * 12)
+    np.testing.assert_allclose(lsk.update_alpha(c, lsk.make_distribution([1.0] * 4), np.zeros(4, np.float32), 0.3),
+                               0.7, rtol=1e-6)
+    w4 = lsk.make_distribution([1.0] * 4)
+    c4 = lsk.make_cost_matrix(4, 4, [0.3] * 16)
+    v = lsk.transport_cost(c4, w4, w4, np.full(4, 0.3, np.float32), np.zeros(4, np.float32), 0.1)
+    assert v == pytest.approx(0.3, rel=1e-6)
+
+
+def test_bit_identical_repeats(cuda_ok):
+    """Determinism contract (reference tests/test_solver.py:247-257)."""
+    mu_w, nu_w, C64 = O.grid_problem(128, 128, 3)
+    cfg = lsk.SinkhornConfig(epsilon=0.01)
+    r1, p1 = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), cfg)
+    r2, p2 = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), cfg)
+    assert r1.iterations == r2.iterations and r1.error_trace == r2.error_trace
+    assert r1.transport_cost == r2.transport_cost
+    np.testing.assert_array_equal(p1.alpha, p2.alpha)
+    np.testing.assert_array_equal(p1.beta, p2.beta)
+
+
+def test_transpose_flag_is_bit_neutral(cuda_ok):
+    mu_w, nu_w, C64 = O.grid_problem(96, 96, 4)
+    r1, p1 = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), lsk.SinkhornConfig(epsilon=0.01))
+    r2, p2 = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w),
+                       lsk.SinkhornConfig(epsilon=0.01, transpose_for_beta=True))
+    assert r1.transport_cost == r2.transport_cost
+    np.testing.assert_array_equal(p1.alpha, p2.alpha)
+
+
+def test_live_oracle_ragged(cuda_ok):
+    """Fresh ragged shapes (n < #SMs, m % 4 != 0, m > n) vs the oracle run now."""
+    for (n, m, eps, seed) in [(7, 3, 0.2, 1), (150, 9, 0.05, 2), (149, 2047, 0.02, 3), (513, 4095, 0.01, 4)]:
+        C64, mu_w, nu_w, _, _ = O.random_problem(n, m, seed)
+        K = 43
+        r = O.solve(C64, mu_w, nu_w, eps, tol=1e-30, max_iter=K, check=10)
+        rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w),
+                             lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K))
+        assert rep.iterations == K and [k for k, _ in rep.error_trace] == [10, 20, 30, 40, 43]
+        assert rel_max(pot.alpha, r["alpha"]) <= RTOL and rel_max(pot.beta, r["beta"]) <= RTOL
+        assert abs(rep.transport_cost - r["cost"]) <= RTOL * abs(r["cost"])
+
+
+def test_device_tensor_cost_and_outputs(cuda_ok):
+    import torch
+
+    mu_w, nu_w, C64 = O.grid_problem(200, 300, 1)
+    Ct = torch.from_numpy(C64).to("cuda", torch.float32)
+    cfg = lsk.SinkhornConfig(epsilon=0.02, max_iterations=50, tolerance=1e-30)
+    r1, p1 = lsk.solve(lsk.CostMatrix(values=Ct), dist(mu_w), dist(nu_w), cfg, return_device=True)
+    r2, p2 = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), cfg)
+    assert p1.alpha.is_cuda
+    np.testing.assert_array_equal(p1.alpha.cpu().numpy(), p2.alpha)
