@@ -229,10 +229,10 @@ def update_alpha(cost, nu, beta, eps, plan=ReductionPlan()):
     _check_precision(beta)
     torch = _half_inputs(cost, eps)
     C = to_device_cost(cost)
-    b = _dev_f32(torch, beta)
+    b, lnu = _vecs(torch, beta, nu.log_weights)
     out = torch.empty(C.rows, dtype=torch.float32, device="cuda")
-    _lib.call("lsk_update_alpha_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(b),
-              _ptr(_dev_f32(torch, nu.log_weights)), float(eps), _ptr(out), _stream_ptr(torch))
+    _lib.call("lsk_update_alpha_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(b), _ptr(lnu), float(eps),
+              _ptr(out), _stream_ptr(torch))
     return out.cpu().numpy()
 
 
@@ -250,14 +250,19 @@ def update_beta(cost, mu, alpha, eps, plan=ReductionPlan(), transposed_cost=None
         shp = tuple(np.shape(transposed_cost)) if not hasattr(transposed_cost, "shape") else tuple(transposed_cost.shape)
         if shp != (C.cols, C.rows):
             raise DimensionMismatch(f"transposed_cost has shape {shp}, expected {(C.cols, C.rows)}")
-    a = _dev_f32(torch, alpha)
+    a, lmu = _vecs(torch, alpha, mu.log_weights)
     out = torch.empty(C.cols, dtype=torch.float32, device="cuda")
     wsb = _lib.load().lsk_update_beta_workspace_bytes(C.rows, C.cols)
     ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
-    _lib.call("lsk_update_beta_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(a),
-              _ptr(_dev_f32(torch, mu.log_weights)), float(eps), _ptr(out), _ptr(ws), ws.numel(),
-              _stream_ptr(torch))
+    _lib.call("lsk_update_beta_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(a), _ptr(lmu), float(eps),
+              _ptr(out), _ptr(ws), ws.numel(), _stream_ptr(torch))
     return out.cpu().numpy()
+
+
+def _vecs(torch, *xs):
+    """fp32 device copies, returned together so they stay alive (and distinct
+    allocations) until the kernel that reads them has been enqueued."""
+    return [_dev_f32(torch, x) for x in xs]
 
 
 def marginal_error(cost, mu, nu, alpha, beta, eps, plan=ReductionPlan()):
@@ -265,12 +270,11 @@ def marginal_error(cost, mu, nu, alpha, beta, eps, plan=ReductionPlan()):
     _check_precision(alpha, beta)
     torch = _half_inputs(cost, eps)
     C = to_device_cost(cost)
+    w, lmu, lnu, a, b = _vecs(torch, mu.weights, mu.log_weights, nu.log_weights, alpha, beta)
     ws = torch.empty(C.rows, dtype=torch.float32, device="cuda")
     out = torch.empty(1, dtype=torch.float32, device="cuda")
-    _lib.call("lsk_marginal_error_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(_dev_f32(torch, mu.weights)),
-              _ptr(_dev_f32(torch, mu.log_weights)), _ptr(_dev_f32(torch, nu.log_weights)),
-              _ptr(_dev_f32(torch, alpha)), _ptr(_dev_f32(torch, beta)), float(eps), _ptr(out), _ptr(ws),
-              ws.numel() * 4, _stream_ptr(torch))
+    _lib.call("lsk_marginal_error_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(w), _ptr(lmu), _ptr(lnu),
+              _ptr(a), _ptr(b), float(eps), _ptr(out), _ptr(ws), ws.numel() * 4, _stream_ptr(torch))
     return float(out.cpu().numpy()[0])
 
 
@@ -279,12 +283,11 @@ def transport_cost(cost, mu, nu, alpha, beta, eps, plan=ReductionPlan()):
     _check_precision(alpha, beta)
     torch = _half_inputs(cost, eps)
     C = to_device_cost(cost)
+    lmu, lnu, a, b = _vecs(torch, mu.log_weights, nu.log_weights, alpha, beta)
     ws = torch.empty(C.rows, dtype=torch.float32, device="cuda")
     out = torch.empty(1, dtype=torch.float32, device="cuda")
-    _lib.call("lsk_transport_cost_f32", _ptr(C.data), C.ldc, C.rows, C.cols,
-              _ptr(_dev_f32(torch, mu.log_weights)), _ptr(_dev_f32(torch, nu.log_weights)),
-              _ptr(_dev_f32(torch, alpha)), _ptr(_dev_f32(torch, beta)), float(eps), _ptr(out), _ptr(ws),
-              ws.numel() * 4, _stream_ptr(torch))
+    _lib.call("lsk_transport_cost_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(lmu), _ptr(lnu), _ptr(a),
+              _ptr(b), float(eps), _ptr(out), _ptr(ws), ws.numel() * 4, _stream_ptr(torch))
     return float(out.cpu().numpy()[0])
 
 
@@ -296,12 +299,11 @@ def materialize_plan(cost, mu, nu, alpha, beta, eps, *, return_device=False):
     _check_precision(alpha, beta)
     torch = _half_inputs(cost, eps)
     C = to_device_cost(cost)
+    lmu, lnu, a, b = _vecs(torch, mu.log_weights, nu.log_weights, alpha, beta)
     P = torch.empty((C.rows, C.cols), dtype=torch.float32, device="cuda")
     bad = torch.zeros(1, dtype=torch.int32, device="cuda")
-    _lib.call("lsk_materialize_plan_f32", _ptr(C.data), C.ldc, C.rows, C.cols,
-              _ptr(_dev_f32(torch, mu.log_weights)), _ptr(_dev_f32(torch, nu.log_weights)),
-              _ptr(_dev_f32(torch, alpha)), _ptr(_dev_f32(torch, beta)), float(eps), _ptr(P), C.cols,
-              _ptr(bad), _stream_ptr(torch))
+    _lib.call("lsk_materialize_plan_f32", _ptr(C.data), C.ldc, C.rows, C.cols, _ptr(lmu), _ptr(lnu), _ptr(a),
+              _ptr(b), float(eps), _ptr(P), C.cols, _ptr(bad), _stream_ptr(torch))
     if int(bad.item()) != 0:
         raise NonFiniteResult("transport plan contains non-finite entries")
     return TransportPlan(values=P if return_device else P.cpu().numpy())
