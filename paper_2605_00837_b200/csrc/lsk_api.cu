@@ -49,10 +49,10 @@ int num_sms() {
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ---- persistent dense solver instances: (NT, V, R, STAGES) by row capacity W
-using Solver1k = lsk::DenseSolver<256, 1, 4, 8>;
-using Solver2k = lsk::DenseSolver<512, 1, 4, 6>;
-using Solver4k = lsk::DenseSolver<512, 2, 2, 6>;
-using Solver8k = lsk::DenseSolver<512, 4, 1, 6>;
+using Solver1k = lsk::DenseSolver<256, 1, 16>;
+using Solver2k = lsk::DenseSolver<512, 1, 16>;
+using Solver4k = lsk::DenseSolver<512, 2, 12>;
+using Solver8k = lsk::DenseSolver<512, 4, 6>;
 
 template <class SV>
 __global__ void __launch_bounds__(SV::NW * 32, 1) k_solve_dense(lsk::DenseArgs a) {

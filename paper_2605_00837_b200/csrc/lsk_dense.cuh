@@ -8,27 +8,29 @@
 // (solver.py:76-115) over reduction.py:179-224.
 //
 // Data layout and schedule:
-//  * CTA b owns rows [b*n/G, (b+1)*n/G). Thread t owns columns
-//    j = 4*(v*NT + t) + q (v < V, q < 4) for the whole solve, so per-column
-//    state (g_j, log nu_j, the column shift, the column accumulator) lives in
-//    registers and each smem row read is one conflict-free LDS.128 per v.
+//  * CTA b owns rows [b*n/G, (b+1)*n/G) for the whole solve. Thread t owns
+//    columns j = 4*(v*NT + t) + q (v < V, q < 4), so per-column state (g_j,
+//    log nu_j, the column shift, the column accumulator) lives in registers as
+//    packed fp32 pairs and each smem row read is a conflict-free 16-byte LDS.
 //  * Rows stream HBM -> smem through a STAGES-deep ring of TMA bulk copies
-//    (cp.async.bulk + mbarrier complete_tx). Each pass alternates the sweep
-//    direction, so the rows read last by one pass are L2-hot for the next.
-//  * ONE pass over C per iteration: from the on-chip row the CTA computes
-//    f_i^k (row LSE against g^{k-1}), then -- from the same registers --
-//    adds exp(y_ij - s_j) into its per-column accumulators, where
+//    (cp.async.bulk + mbarrier complete_tx) that runs ahead across passes.
+//    Passes alternate the sweep direction, so the rows one pass read last are
+//    still L2-resident when the next pass starts.
+//  * ONE pass over C per iteration (fused_pass): from the on-chip row the CTA
+//    computes f_i^k (row LSE against g^{k-1}, shifted by the stale row shift
+//    fl(-f_i^{k-1} * inv_eps)), and one step later -- once the row sum is
+//    known -- adds exp(y_ij - s_j) into its per-column accumulators, where
 //    y_ij = fl(fl(fl(f_i^k - C_ij) * inv_eps) + log mu_i) is the reference's
-//    beta argument and s_j = fl(-g_j^{k-1} * inv_eps) a stale shift
-//    (the terms are bounded by mu_i / nu_j, so no overflow). A
-//    grid-wide combine sums the G partials per column in a fixed tree and
-//    forms g^k. The row LSE uses the stale row shift fl(-f_i^{k-1}*inv_eps)
-//    likewise. Sums outside [1e-20, 1e30] fall back to the exact max shift
-//    (rows: in registers; columns: an exact (max, sumexp) column pass).
-//  * Every c iterations the row pass of k+1 also evaluates the reference
-//    marginal-error formula for iterate k (solver.py:97-104) from the same
-//    on-chip row -- no extra HBM pass, no host sync; f/g are double
-//    buffered so a stop at k returns iterate k.
+//    beta argument and s_j = fl(-g_j^{k-1} * inv_eps) the stale column shift
+//    (terms are bounded by mu_i / nu_j, no overflow). The row LSE
+//    of row q and the column update of row q-1 share one __syncthreads.
+//    A grid-wide fixed-order combine of the G per-CTA column partials forms
+//    g^k. Sums outside [1e-20, 1e30] fall back to the exact max shift (rows:
+//    from the smem copy of the row; columns: an exact (max, sumexp) pass).
+//  * Every c iterations the pass of k+1 also evaluates the reference marginal
+//    error formula for iterate k (solver.py:97-104) from the same on-chip row
+//    -- no extra HBM pass, no host sync; f/g are double buffered so a stop at
+//    k returns iterate k.
 #pragma once
 #include "lsk_device.cuh"
 
@@ -66,15 +68,19 @@ struct DenseArgs {
   int* n_trace;
 };
 
-enum PassKind { kPassRow = 0, kPassColExact = 1, kPassCheck = 2, kPassCost = 3 };
-
-template <int NT, int V, int R, int STAGES>
+template <int NT, int V, int STAGES>
 struct DenseSolver {
   static constexpr int E = 4 * V;       // columns per thread
+  static constexpr int P2 = 2 * V;      // packed pairs per thread
   static constexpr int W = 4 * V * NT;  // row capacity (floats)
   static constexpr int NW = NT / 32;
-  static constexpr size_t kRingBytes = size_t(STAGES) * R * W * sizeof(float);
-  static constexpr size_t kRedFloats = 64 * 2 * R + 64 + NW * 64;
+  static constexpr size_t kRingBytes = size_t(STAGES) * W * sizeof(float);
+  // red layout (floats): [0, 4NW) double-buffered row sums (f, check);
+  // [4NW, 4NW+128) exact-path block reductions; [4NW+128, +64NW) combines
+  static constexpr int kRedRows = 0;
+  static constexpr int kRedExact = 4 * NW;
+  static constexpr int kRedComb = 4 * NW + 128;
+  static constexpr size_t kRedFloats = 4 * NW + 128 + 64 * NW;
   static constexpr size_t kSmemBytes = kRingBytes + kRedFloats * sizeof(float) + STAGES * 8 + 64;
 
   // ---- per-CTA state
@@ -82,13 +88,21 @@ struct DenseSolver {
   float* ring;
   float* red;
   uint64_t* mbar;
-  int b, G, r0, r1, rows, nb;     // rows of this CTA, batches per pass
-  long long issued, consumed;     // global batch counters of the TMA ring
+  int b, G, r0, r1, rows;
+  // TMA ring, tracked incrementally (no 64-bit div/mod on the hot path):
+  // the producer (thread 0) walks the global row sequence pass by pass; the
+  // consumers wait rows in the same order (head) and release them in order (tail).
+  int iss_st, iss_pass, iss_step;  // next row to issue
+  int head_st, head_ph;            // next row to wait for
   unsigned epoch;
-  int pass;                       // pass counter (sweep direction = pass & 1)
+  int pass;                        // pass counter (sweep direction = pass & 1)
+  f2 inv2, l2e2;
 
-  // ---- per-thread column state
-  float gcol[E], lnu[E], gsl[E], acc[E];
+  // ---- per-thread column state (packed pairs of the columns it owns)
+  f2 g2[P2];   // g_j^{k-1}
+  f2 ln2[P2];  // log nu_j (-inf beyond m)
+  f2 ns2[P2];  // -fl(fl(-g_j * inv_eps) * log2e): stale column shift, negated
+  f2 ac2[P2];  // column accumulators
 
   __device__ DenseSolver(const DenseArgs& args, unsigned char* smem) : a(args) {
     ring = reinterpret_cast<float*>(smem);
@@ -99,37 +113,29 @@ struct DenseSolver {
     r0 = int((long long)b * a.n / G);
     r1 = int((long long)(b + 1) * a.n / G);
     rows = r1 - r0;
-    nb = (rows + R - 1) / R;
-    issued = consumed = 0;
+    iss_st = iss_pass = iss_step = 0;
+    head_st = head_ph = 0;
     epoch = 0;
     pass = 0;
+    inv2 = pk2(a.inv_eps, a.inv_eps);
+    l2e2 = pk2(kLog2e, kLog2e);
   }
 
   __device__ __forceinline__ int col(int v, int q) const { return 4 * (v * NT + threadIdx.x) + q; }
+  // row processed at step q of pass P (passes alternate the sweep direction)
+  __device__ __forceinline__ int row_of(int P, int q) const { return (P & 1) ? (r1 - 1 - q) : (r0 + q); }
 
-  // row index of slot r of within-pass batch qb in pass P
-  __device__ __forceinline__ int row_of(int P, int qb, int r) const {
-    int idx = qb * R + r;
-    if (idx >= rows) return -1;
-    return (P & 1) ? (r1 - 1 - idx) : (r0 + idx);
-  }
-
-  // producer (thread 0): issue global batch p into its ring stage
-  __device__ void issue(long long p) {
-    const int st = int(p % STAGES);
-    const int P = int(p / nb), qb = int(p % nb);
+  // ---------------- TMA ring
+  __device__ __forceinline__ void issue() {
     const uint32_t bytes = uint32_t(a.mpad) * 4u;
-    int cnt = 0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) cnt += row_of(P, qb, r) >= 0;
-    mbar_expect_tx(&mbar[st], bytes * cnt);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      int i = row_of(P, qb, r);
-      if (i >= 0) tma_load_1d(ring + (size_t(st) * R + r) * W, a.C + (long long)i * a.ldc, bytes, &mbar[st]);
-    }
+    const int i = row_of(iss_pass, iss_step);
+    mbar_expect_tx(&mbar[iss_st], bytes);
+    tma_load_1d(ring + size_t(iss_st) * W, a.C + (long long)i * a.ldc, bytes, &mbar[iss_st]);
   }
-
+  __device__ __forceinline__ void advance_issue() {
+    iss_st = (iss_st + 1 == STAGES) ? 0 : iss_st + 1;
+    if (++iss_step == rows) { iss_step = 0; ++iss_pass; }
+  }
   __device__ void ring_init() {
     // zero the ring once: columns >= mpad are never written by TMA and must read as 0
     float4* r4 = reinterpret_cast<float4*>(ring);
@@ -139,269 +145,407 @@ struct DenseSolver {
       fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0 && nb > 0) {
-      fence_proxy_async();
-      for (; issued < STAGES; ++issued) issue(issued);
+    if (threadIdx.x == 0) fence_proxy_async();
+    for (int s = 0; s < STAGES; ++s) {
+      if (threadIdx.x == 0) issue();
+      advance_issue();
     }
   }
-
-  // wait for batch `consumed`, copy the R rows of this thread's columns to regs
-  __device__ __forceinline__ void load_batch(float (&c)[R][E]) {
-    const int st = int(consumed % STAGES);
-    mbar_wait(&mbar[st], uint32_t((consumed / STAGES) & 1));
-    const float* base = ring + size_t(st) * R * W;
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int v = 0; v < V; ++v) {
-        float4 t4 = reinterpret_cast<const float4*>(base + size_t(r) * W)[v * NT + threadIdx.x];
-        c[r][4 * v + 0] = t4.x; c[r][4 * v + 1] = t4.y; c[r][4 * v + 2] = t4.z; c[r][4 * v + 3] = t4.w;
-      }
+  // wait for the next row of the sequence; returns its smem copy
+  __device__ __forceinline__ const float* wait_head() {
+    mbar_wait(&mbar[head_st], uint32_t(head_ph));
+    const float* p = ring + size_t(head_st) * W;
+    if (++head_st == STAGES) { head_st = 0; head_ph ^= 1; }
+    return p;
   }
-  // call after a __syncthreads that follows load_batch: the stage is free
-  __device__ __forceinline__ void refill() {
+  // release the oldest held row (call after a __syncthreads that follows every
+  // read of it) and refill its stage with the next row of the sequence
+  __device__ __forceinline__ void release() {
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      issue(issued);
-      ++issued;
+      issue();
     }
-    ++consumed;
+    advance_issue();
   }
+  // every stage holds an issued row at the end: wait for all before exit
   __device__ void drain() {
-    if (threadIdx.x == 0)
-      for (long long p = consumed; p < issued; ++p)
-        mbar_wait(&mbar[int(p % STAGES)], uint32_t((p / STAGES) & 1));
+    for (int s = 0; s < STAGES; ++s) wait_head();
     __syncthreads();
   }
 
-  __device__ void load_columns(const float* g) {
+  // this thread's columns of a smem row as packed pairs
+  __device__ __forceinline__ void load_row(const float* base, f2 (&c)[P2]) const {
+#pragma unroll
+    for (int v = 0; v < V; ++v) lds2x2(base + 4 * (v * NT + threadIdx.x), c[2 * v], c[2 * v + 1]);
+  }
+
+  __device__ void load_lognu() {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      int j0 = 4 * (v * NT + threadIdx.x);
-      float4 t4 = j0 < a.m ? ldcg4(reinterpret_cast<const float4*>(g + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float tt[4] = {t4.x, t4.y, t4.z, t4.w};
+      float t[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        float gj = (j0 + q < a.m) ? tt[q] : 0.f;
-        gcol[4 * v + q] = gj;
-        gsl[4 * v + q] = __fmul_rn(__fmul_rn(-gj, a.inv_eps), kLog2e);
-        acc[4 * v + q] = 0.f;
+        const int j = col(v, q);
+        t[q] = j < a.m ? __ldg(a.log_nu + j) : -INFINITY;
       }
+      ln2[2 * v] = pk2(t[0], t[1]);
+      ln2[2 * v + 1] = pk2(t[2], t[3]);
     }
   }
-
-  // ---- the exact (max-shifted) row LSE of the f argument, from registers
-  __device__ __forceinline__ void exact_row(const float (&c)[R][E], int r, float& M, float& S) {
-    float mx[1] = {-INFINITY};
+  // g^{k-1} into registers (+ the stale column shifts); returns "some owned g is non-finite"
+  __device__ bool load_columns(const float* g) {
+    bool bad = false;
 #pragma unroll
-    for (int e = 0; e < E; ++e) mx[0] = fmax_nan(mx[0], arg3(gcol[e], c[r][e], a.inv_eps, lnu[e]));
-    block_reduce<NT, 1, true>(mx, red + 64 * 2 * R);
-    M = mx[0];
-    float Ms = (fabsf(M) <= 3.402823466e38f) ? M : 0.f;
-    float sl = __fmul_rn(Ms, kLog2e);
-    float s[1] = {0.f};
+    for (int v = 0; v < V; ++v) {
+      const int j0 = col(v, 0);
+      float4 t4 = j0 < a.m ? ldcg4(reinterpret_cast<const float4*>(g + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float t[4] = {t4.x, t4.y, t4.z, t4.w};
+      float ns[4];
 #pragma unroll
-    for (int e = 0; e < E; ++e) s[0] += exp_shifted(arg3(gcol[e], c[r][e], a.inv_eps, lnu[e]), sl);
-    __syncthreads();  // red reuse
-    block_reduce<NT, 1, false>(s, red + 64 * 2 * R);
-    S = s[0];
-    __syncthreads();
+      for (int q = 0; q < 4; ++q) {
+        if (j0 + q >= a.m) t[q] = 0.f;
+        bad |= !isfinite(t[q]);
+        ns[q] = -__fmul_rn(__fmul_rn(-t[q], a.inv_eps), kLog2e);
+      }
+      g2[2 * v] = pk2(t[0], t[1]);
+      g2[2 * v + 1] = pk2(t[2], t[3]);
+      ns2[2 * v] = pk2(ns[0], ns[1]);
+      ns2[2 * v + 1] = pk2(ns[2], ns[3]);
+      ac2[2 * v] = 0ull;
+      ac2[2 * v + 1] = 0ull;
+    }
+    return bad;
   }
-  __device__ __forceinline__ void exact_check_row(const float (&c)[R][E], int r, float fi, float& M, float& S) {
-    float mx[1] = {-INFINITY};
-#pragma unroll
-    for (int e = 0; e < E; ++e) mx[0] = fmax_nan(mx[0], arg4(fi, gcol[e], c[r][e], a.inv_eps, lnu[e]));
-    block_reduce<NT, 1, true>(mx, red + 64 * 2 * R);
-    M = mx[0];
-    float Ms = (fabsf(M) <= 3.402823466e38f) ? M : 0.f;
-    float sl = __fmul_rn(Ms, kLog2e);
-    float s[1] = {0.f};
-#pragma unroll
-    for (int e = 0; e < E; ++e) s[0] += exp_shifted(arg4(fi, gcol[e], c[r][e], a.inv_eps, lnu[e]), sl);
+
+  // ---------------- block reductions for the exact (max-shifted) paths
+  __device__ __forceinline__ float block_max1(float v) {
+    float t[1] = {v};
+    block_reduce<NT, 1, true>(t, red + kRedExact);
     __syncthreads();
-    block_reduce<NT, 1, false>(s, red + 64 * 2 * R);
-    S = s[0];
+    return t[0];
+  }
+  __device__ __forceinline__ float block_sum1(float v) {
+    float t[1] = {v};
+    block_reduce<NT, 1, false>(t, red + kRedExact);
     __syncthreads();
+    return t[0];
+  }
+  // exact LSE of the f argument arg3(g_j, C_ij, inv, lnu_j) over a smem row
+  __device__ void exact_row(const float* row, float& M, float& S) {
+    f2 c[P2];
+    load_row(row, c);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int p = 0; p < P2; ++p) {
+      float x0, x1;
+      up2(arg3x2(g2[p], c[p], inv2, ln2[p]), x0, x1);
+      mx = fmax_nan(mx, fmax_nan(x0, x1));
+    }
+    M = block_max1(mx);
+    const float Ms = (fabsf(M) <= 3.402823466e38f) ? M : 0.f;
+    const f2 nsl = pk2(-__fmul_rn(Ms, kLog2e), -__fmul_rn(Ms, kLog2e));
+    f2 s2 = 0ull;
+#pragma unroll
+    for (int p = 0; p < P2; ++p) s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p]), l2e2, nsl)));
+    float s0, s1;
+    up2(s2, s0, s1);
+    S = block_sum1(s0 + s1);
+  }
+  // exact LSE of the check argument arg4(f_i, g_j, C_ij, inv, lnu_j) over a smem row
+  __device__ void exact_check_row(const float* row, float fi, float& M, float& S) {
+    f2 c[P2];
+    load_row(row, c);
+    const f2 f2i = pk2(fi, fi);
+    float mx = -INFINITY;
+#pragma unroll
+    for (int p = 0; p < P2; ++p) {
+      float x0, x1;
+      up2(arg4x2(f2i, g2[p], c[p], inv2, ln2[p]), x0, x1);
+      mx = fmax_nan(mx, fmax_nan(x0, x1));
+    }
+    M = block_max1(mx);
+    const float Ms = (fabsf(M) <= 3.402823466e38f) ? M : 0.f;
+    const f2 nsl = pk2(-__fmul_rn(Ms, kLog2e), -__fmul_rn(Ms, kLog2e));
+    f2 s2 = 0ull;
+#pragma unroll
+    for (int p = 0; p < P2; ++p) s2 = add2(s2, ex2x2(fma2(arg4x2(f2i, g2[p], c[p], inv2, ln2[p]), l2e2, nsl)));
+    float s0, s1;
+    up2(s2, s0, s1);
+    S = block_sum1(s0 + s1);
   }
 
   static __device__ __forceinline__ bool shift_ok(float S) { return S >= kShiftLo && S <= kShiftHi; }
 
-  // ---- one streaming pass over this CTA's rows
-  // kPassRow:      f^k from g^{k-1} (gcol), stale column partials into acc,
-  //                optionally the marginal check of iterate k-1 (fchk = f^{k-1})
-  // kPassColExact: exact (max, sumexp) of the beta argument per column (acc=max, gsl=sum)
-  // kPassCheck:    marginal check only (fchk = f^k, gcol = g^k)
-  // kPassCost:     transport cost (fchk = f, gcol = g)
-  template <int KIND>
-  __device__ void run_pass(const float* fprev, float* fnew, bool exact_rows, bool do_check,
-                           float& err_acc, int& bad_flag, float& cost_acc, bool do_gpart = false) {
-    const int P = pass++;
-    if (nb == 0) return;
-    float c[R][E];
-    for (int qb = 0; qb < nb; ++qb) {
-      load_batch(c);
-      int ri[R];
-      float fold[R], lmu_r[R];
+  // fixed-order sum of the NW warp partials at red[off .. off+NW) (same bits in every thread)
+  __device__ __forceinline__ float sum_warps(int off) const {
+    float s = 0.f;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        ri[r] = row_of(P, qb, r);
-        int i = ri[r] < 0 ? r0 : ri[r];
-        fold[r] = ldcg(fprev + i);
-        lmu_r[r] = __ldg(a.log_mu + i);
-      }
-      if (KIND == kPassRow) {
-        // --- f-update (+ check) sums
-        float S[2 * R];
-        float sh[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          sh[r] = exact_rows ? 0.f : __fmul_rn(-fold[r], a.inv_eps);
-          S[r] = 0.f;
-          S[R + r] = 0.f;
-        }
-        if (!exact_rows) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float sl = __fmul_rn(sh[r], kLog2e);
-            float s = 0.f, sz = 0.f;
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              s += exp_shifted(arg3(gcol[e], c[r][e], a.inv_eps, lnu[e]), sl);
-              if (do_check) sz += ex2(__fmul_rn(arg4(fold[r], gcol[e], c[r][e], a.inv_eps, lnu[e]), kLog2e));
-            }
-            S[r] = s;
-            S[R + r] = sz;
-          }
-          if (do_check) block_reduce<NT, 2 * R, false>(S, red);
-          else {
-            float S1[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) S1[r] = S[r];
-            block_reduce<NT, R, false>(S1, red);
-#pragma unroll
-            for (int r = 0; r < R; ++r) S[r] = S1[r];
-          }
-        } else {
-          if (do_check) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              float sz = 0.f;
-#pragma unroll
-              for (int e = 0; e < E; ++e)
-                sz += ex2(__fmul_rn(arg4(fold[r], gcol[e], c[r][e], a.inv_eps, lnu[e]), kLog2e));
-              S[R + r] = sz;
-            }
-            float S2[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) S2[r] = S[R + r];
-            block_reduce<NT, R, false>(S2, red);
-#pragma unroll
-            for (int r = 0; r < R; ++r) S[R + r] = S2[r];
-          } else {
-            __syncthreads();
-          }
-        }
-        refill();
-        __syncthreads();  // red consumed before any exact-path reuse
-        float fr[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float M = sh[r], Ssum = S[r];
-          if (exact_rows || !shift_ok(Ssum)) {
-            if (!exact_rows && threadIdx.x == 0 && ri[r] >= 0) atomicAdd(a.stats + 0, 1);
-            exact_row(c, r, M, Ssum);
-          }
-          fr[r] = __fmul_rn(a.neg_eps, lse_finish(M, Ssum));
-          if (do_check) {
-            float Mz = 0.f, Sz = S[R + r];
-            if (!shift_ok(Sz)) exact_check_row(c, r, fold[r], Mz, Sz);
-            float L = lse_finish(Mz, Sz);
-            float rr = expf(__fadd_rn(lmu_r[r], L));
-            if (threadIdx.x == 0 && ri[r] >= 0) {
-              err_acc += fabsf(__fsub_rn(rr, __ldg(a.mu + ri[r])));
-              if (!isfinite(fold[r])) bad_flag = 1;
-            }
-          }
-          if (threadIdx.x == 0 && ri[r] >= 0) fnew[ri[r]] = fr[r];
-        }
-        // --- stale-shift column partials of the beta argument, same registers
-        if (do_gpart)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (ri[r] < 0) continue;
-#pragma unroll
-          for (int e = 0; e < E; ++e) acc[e] += exp_shifted(arg3(fr[r], c[r][e], a.inv_eps, lmu_r[r]), gsl[e]);
-        }
-      } else if (KIND == kPassColExact) {
-        // chunked online (max, sumexp) per owned column; acc = max, gsl = sum
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          float y[R];
-          float cm = -INFINITY;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            y[r] = ri[r] >= 0 ? arg3(fold[r], c[r][e], a.inv_eps, lmu_r[r]) : -INFINITY;
-            cm = fmax_nan(cm, y[r]);
-          }
-          float mo = acc[e];
-          float mn = fmax_nan(mo, cm);
-          float ms = (fabsf(mn) <= 3.402823466e38f) ? mn : 0.f;
-          float sl = __fmul_rn(ms, kLog2e);
-          float s = (mo == -INFINITY) ? 0.f : gsl[e] * exp_shifted(mo, sl);
-#pragma unroll
-          for (int r = 0; r < R; ++r) s += exp_shifted(y[r], sl);
-          acc[e] = mn;
-          gsl[e] = s;
-        }
-        __syncthreads();
-        refill();
-      } else if (KIND == kPassCheck) {
-        float S[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float sz = 0.f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) sz += ex2(__fmul_rn(arg4(fold[r], gcol[e], c[r][e], a.inv_eps, lnu[e]), kLog2e));
-          S[r] = sz;
-        }
-        block_reduce<NT, R, false>(S, red);
-        refill();
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float Mz = 0.f, Sz = S[r];
-          if (!shift_ok(Sz)) exact_check_row(c, r, fold[r], Mz, Sz);
-          float L = lse_finish(Mz, Sz);
-          float rr = expf(__fadd_rn(lmu_r[r], L));
-          if (threadIdx.x == 0 && ri[r] >= 0) {
-            err_acc += fabsf(__fsub_rn(rr, __ldg(a.mu + ri[r])));
-            if (!isfinite(fold[r])) bad_flag = 1;
-          }
-        }
-      } else {  // kPassCost: sum_ij fl(C_ij * exp(z_ij)), z as solver.py:108-112
-        float S[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float s = 0.f;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            float z = __fadd_rn(arg4(fold[r], gcol[e], c[r][e], a.inv_eps, lmu_r[r]), lnu[e]);
-            s += __fmul_rn(c[r][e], expf(z));
-          }
-          S[r] = ri[r] >= 0 ? s : 0.f;
-        }
-        block_reduce<NT, R, false>(S, red);
-        refill();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) cost_acc += S[r];
-        }
-      }
+    for (int w = 0; w < NW; w += 4) {
+      const float4 t = *reinterpret_cast<const float4*>(red + off + w);
+      s += (t.x + t.y) + (t.z + t.w);
+    }
+    return s;
+  }
+
+  // marginal-check bookkeeping for row i given its check sum (shift 0)
+  __device__ __forceinline__ void check_row(const float* row, int i, float fold, float lmu, float Sz,
+                                            float& err_acc, int& bad) {
+    float Mz = 0.f;
+    if (!shift_ok(Sz)) exact_check_row(row, fold, Mz, Sz);
+    if (threadIdx.x == 0) {
+      const float rr = expf(__fadd_rn(lmu, lse_finish(Mz, Sz)));
+      err_acc += fabsf(__fsub_rn(rr, __ldg(a.mu + i)));
+      if (!isfinite(fold)) bad = 1;
     }
   }
 
-  // fixed-order tree over the G per-CTA scalars (identical in every CTA)
+  // ================= the fused one-pass iteration (stale shifts) =================
+  // f^k = neg_eps * LSE_j(arg3(g_j^{k-1}, C_ij)) for this CTA's rows, written to
+  // fnew; stale-shift column partials of the beta argument into ac2; with CHECK,
+  // the marginal error of iterate k-1 (fold = f^{k-1}, g2 = g^{k-1}).
+  //
+  // Software pipeline, one __syncthreads per row: step q computes the per-thread
+  // row sums of row q, then the column update of row q-1 (whose f is known)
+  // with the warp butterfly of row q's sums interleaved into it, then the
+  // barrier, then every thread finishes row q from the NW warp sums.
+
+  // per-thread partial sums of row `row` (f argument, and the check argument)
+  template <bool CHECK>
+  __device__ __forceinline__ void f_part(const float* row, float fold, float& s, float& z) const {
+    f2 c[P2];
+    load_row(row, c);
+    const float shl = __fmul_rn(__fmul_rn(-fold, a.inv_eps), kLog2e);
+    const f2 nsl = pk2(-shl, -shl);
+    const f2 fo2 = pk2(fold, fold);
+    f2 s2 = 0ull, z2 = 0ull;
+#pragma unroll
+    for (int p = 0; p < P2; ++p) {
+      s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p]), l2e2, nsl)));
+      if (CHECK) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p]), l2e2)));
+    }
+    float s0, s1;
+    up2(s2, s0, s1);
+    s = s0 + s1;
+    if (CHECK) {
+      up2(z2, s0, s1);
+      z = s0 + s1;
+    }
+  }
+  // column update of row `row` with its fresh f; the 5 butterfly levels of the
+  // pending row sums (s, z) are interleaved so their latency hides under MUFU work
+  template <bool CHECK, bool SHFL>
+  __device__ __forceinline__ void g_part(const float* row, float fi, float lmu, float& s, float& z) {
+    f2 c[P2];
+    load_row(row, c);
+    const f2 fi2 = pk2(fi, fi), lm2 = pk2(lmu, lmu);
+#pragma unroll
+    for (int p = 0; p < P2; ++p) {
+      ac2[p] = add2(ac2[p], ex2x2(fma2(arg3x2(fi2, c[p], inv2, lm2), l2e2, ns2[p])));
+      if (SHFL && p < 5) {
+        s += __shfl_xor_sync(0xffffffffu, s, 16 >> p);
+        if (CHECK) z += __shfl_xor_sync(0xffffffffu, z, 16 >> p);
+      }
+    }
+    if (SHFL)
+#pragma unroll
+      for (int l = P2; l < 5; ++l) {
+        s += __shfl_xor_sync(0xffffffffu, s, 16 >> l);
+        if (CHECK) z += __shfl_xor_sync(0xffffffffu, z, 16 >> l);
+      }
+  }
+  // after the barrier: finish row i from the warp sums in red[(q&1)]
+  template <bool CHECK>
+  __device__ __forceinline__ float f_finish(const float* row, int q, int i, float fold, float lmu, float* fnew,
+                                            float& err_acc, int& bad) {
+    float M = __fmul_rn(-fold, a.inv_eps), S = sum_warps(kRedRows + (q & 1) * NW);
+    if (!shift_ok(S)) {  // uniform: every thread holds the same S
+      if (threadIdx.x == 0) atomicAdd(a.stats + 0, 1);
+      exact_row(row, M, S);
+    }
+    // accurate logf: lg2.approx moves f by ~1e-7 relative, which shifts the
+    // marginal error near the fp32 floor enough to flip converged/not_converged
+    // against the reference at err ~ tol (tests: grid64_check5)
+    const float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
+    if (CHECK) check_row(row, i, fold, lmu, sum_warps(kRedRows + 2 * NW + (q & 1) * NW), err_acc, bad);
+    if (threadIdx.x == 0) fnew[i] = fr;
+    return fr;
+  }
+
+  template <bool CHECK>
+  __device__ void fused_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
+    const int P = pass++;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // scalars of the current row and (prefetched) of the next one
+    int i = row_of(P, 0);
+    float fold = ldcg(fprev + i), lmu = __ldg(a.log_mu + i);
+    int i_nx = i;
+    float fold_nx = fold, lmu_nx = lmu;
+    if (rows > 1) {
+      i_nx = row_of(P, 1);
+      fold_nx = ldcg(fprev + i_nx);
+      lmu_nx = __ldg(a.log_mu + i_nx);
+    }
+    // step 0: row sums of row 0 only
+    const float* row = wait_head();
+    float s, z = 0.f;
+    f_part<CHECK>(row, fold, s, z);
+    s = warp_sum(s);
+    if (CHECK) z = warp_sum(z);
+    if (lane == 0) {
+      red[kRedRows + w] = s;
+      if (CHECK) red[kRedRows + 2 * NW + w] = z;
+    }
+    __syncthreads();
+    float f_prev = f_finish<CHECK>(row, 0, i, fold, lmu, fnew, err_acc, bad);
+    float lmu_prev = lmu;
+    const float* row_prev = row;
+    for (int q = 1; q < rows; ++q) {
+      i = i_nx; fold = fold_nx; lmu = lmu_nx;
+      if (q + 1 < rows) {
+        i_nx = row_of(P, q + 1);
+        fold_nx = ldcg(fprev + i_nx);
+        lmu_nx = __ldg(a.log_mu + i_nx);
+      }
+      row = wait_head();
+      f_part<CHECK>(row, fold, s, z);
+      g_part<CHECK, true>(row_prev, f_prev, lmu_prev, s, z);
+      if (lane == 0) {
+        red[kRedRows + (q & 1) * NW + w] = s;
+        if (CHECK) red[kRedRows + 2 * NW + (q & 1) * NW + w] = z;
+      }
+      __syncthreads();
+      release();  // row q-1 fully consumed by every thread
+      f_prev = f_finish<CHECK>(row, q, i, fold, lmu, fnew, err_acc, bad);
+      lmu_prev = lmu;
+      row_prev = row;
+    }
+    g_part<false, false>(row_prev, f_prev, lmu_prev, s, z);
+    __syncthreads();
+    release();
+  }
+
+  // ================= exact row pass (two-pass max/sum from the on-chip row) ========
+  template <bool CHECK>
+  __device__ void row_exact_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
+    const int P = pass++;
+    for (int q = 0; q < rows; ++q) {
+      const int i = row_of(P, q);
+      const float* row = wait_head();
+      float M, S;
+      exact_row(row, M, S);
+      const float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
+      if (CHECK) {
+        const float fold = ldcg(fprev + i);
+        const f2 fo2 = pk2(fold, fold);
+        f2 c[P2];
+        load_row(row, c);
+        f2 z2 = 0ull;
+#pragma unroll
+        for (int p = 0; p < P2; ++p) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p]), l2e2)));
+        float s0, s1;
+        up2(z2, s0, s1);
+        const float Sz = block_sum1(s0 + s1);
+        check_row(row, i, fold, __ldg(a.log_mu + i), Sz, err_acc, bad);
+      }
+      if (threadIdx.x == 0) fnew[i] = fr;
+      __syncthreads();
+      release();
+    }
+  }
+
+  // ================= check-only pass (final check at the cap) =================
+  __device__ void check_pass(const float* f, float& err_acc, int& bad) {
+    const int P = pass++;
+    for (int q = 0; q < rows; ++q) {
+      const int i = row_of(P, q);
+      const float* row = wait_head();
+      const float fold = ldcg(f + i);
+      const f2 fo2 = pk2(fold, fold);
+      f2 c[P2];
+      load_row(row, c);
+      f2 z2 = 0ull;
+#pragma unroll
+      for (int p = 0; p < P2; ++p) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p]), l2e2)));
+      float s0, s1;
+      up2(z2, s0, s1);
+      const float Sz = block_sum1(s0 + s1);
+      check_row(row, i, fold, __ldg(a.log_mu + i), Sz, err_acc, bad);
+      __syncthreads();
+      release();
+    }
+  }
+
+  // ================= transport cost: sum_ij fl(C_ij * exp(z_ij)), z as solver.py:108-112
+  __device__ void cost_pass(const float* f, float& cost_acc) {
+    const int P = pass++;
+    for (int q = 0; q < rows; ++q) {
+      const int i = row_of(P, q);
+      const float* row = wait_head();
+      const float fi = ldcg(f + i), lmu = __ldg(a.log_mu + i);
+      const f2 fi2 = pk2(fi, fi), lm2 = pk2(lmu, lmu);
+      f2 c[P2];
+      load_row(row, c);
+      float s = 0.f;
+#pragma unroll
+      for (int p = 0; p < P2; ++p) {
+        const f2 z = add2(arg4x2(fi2, g2[p], c[p], inv2, lm2), ln2[p]);
+        float z0, z1, c0, c1;
+        up2(z, z0, z1);
+        up2(c[p], c0, c1);
+        s += __fmul_rn(c0, expf(z0));
+        s += __fmul_rn(c1, expf(z1));
+      }
+      const float S = block_sum1(s);
+      if (threadIdx.x == 0) cost_acc += S;
+      __syncthreads();
+      release();
+    }
+  }
+
+  // ================= exact column pass: online (max, sumexp) per owned column ======
+  // beta argument arg3(f_i^k, C_ij, inv, log mu_i); writes (max, sum) pairs to a.pairs[b]
+  __device__ void col_exact_pass(const float* f) {
+    const int P = pass++;
+    float cm[E], cs[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { cm[e] = -INFINITY; cs[e] = 0.f; }
+    for (int q = 0; q < rows; ++q) {
+      const int i = row_of(P, q);
+      const float* row = wait_head();
+      const float fi = ldcg(f + i), lmu = __ldg(a.log_mu + i);
+      const f2 fi2 = pk2(fi, fi), lm2 = pk2(lmu, lmu);
+      f2 c[P2];
+      load_row(row, c);
+#pragma unroll
+      for (int p = 0; p < P2; ++p) {
+        float y[2];
+        up2(arg3x2(fi2, c[p], inv2, lm2), y[0], y[1]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = 2 * p + h;
+          const float mo = cm[e];
+          const float mn = fmax_nan(mo, y[h]);
+          const float ms = (fabsf(mn) <= 3.402823466e38f) ? mn : 0.f;
+          const float sl = __fmul_rn(ms, kLog2e);
+          const float s = (mo == -INFINITY) ? 0.f : cs[e] * exp_shifted(mo, sl);
+          cs[e] = s + exp_shifted(y[h], sl);
+          cm[e] = mn;
+        }
+      }
+      __syncthreads();
+      release();
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int j0 = col(v, 0);
+      if (j0 >= a.m) continue;
+      float2* dst = a.pairs + (size_t)b * W + j0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) dst[q] = make_float2(cm[4 * v + q], cs[4 * v + q]);
+    }
+  }
+
+  // ---- fixed-order tree over the G per-CTA scalars (identical in every CTA)
   __device__ float tree_over_ctas(const float* v) {
     const int lane = threadIdx.x & 31;
     float s = 0.f;
@@ -415,27 +559,35 @@ struct DenseSolver {
     return __any_sync(0xffffffffu, s != 0);
   }
 
-  // ---- column combines: CTA b handles 32-column groups b, b+G, ...; the
-  // NW warps split the G partial rows into contiguous ranges, then a fixed
+  // ---- column combines: CTA b handles 32-column groups b, b+G, ...; the NW
+  // warps split the G partial rows into contiguous ranges, then a fixed
   // halving tree over the NW range sums (in smem) finishes each column.
   __device__ void combine_stale(const float* gold, float* gnew, int k) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ngroups = (a.m + 31) / 32;
+    float* cr = red + kRedComb;
     bool fired = false;
     for (int grp = b; grp < ngroups; grp += G) {
       const int j = grp * 32 + lane;
       const int k0 = w * G / NW, k1 = (w + 1) * G / NW;
       float s = 0.f;
-      if (j < a.m)
-        for (int kk = k0; kk < k1; ++kk) s += ldcg(a.part + (size_t)kk * W + j);
-      red[w * 32 + lane] = s;
+      if (j < a.m) {
+        int kk = k0;
+        for (; kk + 4 <= k1; kk += 4) {
+          const float v0 = ldcg(a.part + (size_t)kk * W + j), v1 = ldcg(a.part + (size_t)(kk + 1) * W + j);
+          const float v2 = ldcg(a.part + (size_t)(kk + 2) * W + j), v3 = ldcg(a.part + (size_t)(kk + 3) * W + j);
+          s += (v0 + v1) + (v2 + v3);
+        }
+        for (; kk < k1; ++kk) s += ldcg(a.part + (size_t)kk * W + j);
+      }
+      cr[w * 32 + lane] = s;
       __syncthreads();
       if (w == 0) {
         for (int h = NW / 2; h >= 1; h >>= 1)
-          for (int u = 0; u < h; ++u) red[u * 32 + lane] += red[(u + h) * 32 + lane];
+          for (int u = 0; u < h; ++u) cr[u * 32 + lane] += cr[(u + h) * 32 + lane];
         if (j < a.m) {
-          float sj = __fmul_rn(-ldcg(gold + j), a.inv_eps);
-          float S = red[lane];
+          const float sj = __fmul_rn(-ldcg(gold + j), a.inv_eps);
+          const float S = cr[lane];
           if (!shift_ok(S)) fired = true;
           gnew[j] = __fmul_rn(a.neg_eps, lse_finish(sj, S));
         }
@@ -448,6 +600,7 @@ struct DenseSolver {
   __device__ void combine_pairs(float* gnew) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int ngroups = (a.m + 31) / 32;
+    float* cr = red + kRedComb;
     for (int grp = b; grp < ngroups; grp += G) {
       const int j = grp * 32 + lane;
       const int k0 = w * G / NW, k1 = (w + 1) * G / NW;
@@ -457,42 +610,37 @@ struct DenseSolver {
           float2 p = __ldcg(a.pairs + (size_t)kk * W + j);
           pair_merge(mx, s, p.x, p.y);
         }
-      red[w * 64 + lane] = mx;
-      red[w * 64 + 32 + lane] = s;
+      cr[w * 64 + lane] = mx;
+      cr[w * 64 + 32 + lane] = s;
       __syncthreads();
       if (w == 0) {
         for (int h = NW / 2; h >= 1; h >>= 1)
           for (int u = 0; u < h; ++u) {
-            float m1 = red[u * 64 + lane], s1 = red[u * 64 + 32 + lane];
-            pair_merge(m1, s1, red[(u + h) * 64 + lane], red[(u + h) * 64 + 32 + lane]);
-            red[u * 64 + lane] = m1;
-            red[u * 64 + 32 + lane] = s1;
+            float m1 = cr[u * 64 + lane], s1 = cr[u * 64 + 32 + lane];
+            pair_merge(m1, s1, cr[(u + h) * 64 + lane], cr[(u + h) * 64 + 32 + lane]);
+            cr[u * 64 + lane] = m1;
+            cr[u * 64 + 32 + lane] = s1;
           }
-        if (j < a.m) gnew[j] = __fmul_rn(a.neg_eps, lse_finish(red[lane], red[32 + lane]));
+        if (j < a.m) gnew[j] = __fmul_rn(a.neg_eps, lse_finish(cr[lane], cr[32 + lane]));
       }
       __syncthreads();
     }
   }
 
-  __device__ void store_partials(bool pairs_mode) {
+  __device__ void store_stale_partials() {
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      const int j0 = 4 * (v * NT + threadIdx.x);
-      if (j0 >= a.m) continue;
-      if (pairs_mode) {
-        float2* dst = a.pairs + (size_t)b * W + j0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_float2(acc[4 * v + q], gsl[4 * v + q]);
-      } else {
-        reinterpret_cast<float4*>(a.part + (size_t)b * W)[v * NT + threadIdx.x] =
-            make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
-      }
+      if (col(v, 0) >= a.m) continue;
+      float x0, x1, x2, x3;
+      up2(ac2[2 * v], x0, x1);
+      up2(ac2[2 * v + 1], x2, x3);
+      reinterpret_cast<float4*>(a.part + (size_t)b * W)[v * NT + threadIdx.x] = make_float4(x0, x1, x2, x3);
     }
   }
 
   // ---- check decision, identical in every CTA (solver.py:286-300)
   // returns true if the solve stops at iterate kk
-  __device__ bool decide(int kk, bool& failed, float& err_out) {
+  __device__ bool decide(int kk, bool& failed) {
     const int bad = any_over_ctas(a.flagpart);
     const float err = tree_over_ctas(a.errpart);
     bool stop = false;
@@ -513,62 +661,47 @@ struct DenseSolver {
       *a.out_err = e;
     }
     failed = status == 2;
-    err_out = e;
     return stop;
   }
 
+  __device__ void publish_check(float err_acc, int bad) {
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) { a.errpart[b] = err_acc; a.flagpart[b] = bad; }
+  }
+
   __device__ void solve() {
-    const float* gcur;
-    // per-thread log nu for owned columns (-inf masks columns >= m)
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int j = col(v, q);
-        lnu[4 * v + q] = j < a.m ? __ldg(a.log_nu + j) : -INFINITY;
-      }
+    load_lognu();
     ring_init();
     auto fb = [&](int k) { return (k & 1) ? a.f1 : a.f0; };
     auto gb = [&](int k) { return (k & 1) ? a.g1 : a.g0; };
     int final_k = a.max_iter;
     bool stopped = false, failed = false;
-    float err_dummy = 0.f;
     for (int k = 1; k <= a.max_iter; ++k) {
       const bool do_check = (k > 1) && ((k - 1) % a.check == 0);
-      gcur = gb((k - 1) & 1);
-      load_columns(gcur);
-      float err_acc = 0.f, cost_dummy = 0.f;
-      int bad = 0;
-      if (do_check) {
-        // finiteness of g^{k-1} on this CTA's view (every CTA holds all of g)
-#pragma unroll
-        for (int e = 0; e < E; ++e)
-          if (!isfinite(gcol[e]) && col(e / 4, e % 4) < a.m) bad = 1;
+      const float* gcur = gb((k - 1) & 1);
+      const bool gbad = load_columns(gcur);
+      float err_acc = 0.f;
+      int bad = (do_check && gbad) ? 1 : 0;
+      const bool fused = a.stale && k > 1;
+      if (fused) {
+        if (do_check) fused_pass<true>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
+        else fused_pass<false>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
+        store_stale_partials();
+      } else {
+        if (do_check) row_exact_pass<true>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
+        else row_exact_pass<false>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
       }
-      const bool exact_rows = (k == 1) || !a.stale;
-      run_pass<kPassRow>(fb((k - 1) & 1), fb(k & 1), exact_rows, do_check, err_acc, bad, cost_dummy,
-                         a.stale && k > 1);
-      if (do_check) {
-        bad = __syncthreads_or(bad);
-        if (threadIdx.x == 0) { a.errpart[b] = err_acc; a.flagpart[b] = bad; }
-      }
-      if (a.stale && k > 1) store_partials(false);
+      if (do_check) publish_check(err_acc, bad);
       grid_barrier(a.bar, epoch);
-      if (do_check) {
-        float e;
-        if (decide(k - 1, failed, e)) { stopped = true; final_k = k - 1; break; }
-      }
-      if (a.stale && k > 1) {
+      if (do_check && decide(k - 1, failed)) { stopped = true; final_k = k - 1; break; }
+      if (fused) {
         combine_stale(gcur, gb(k & 1), k);
         grid_barrier(a.bar, epoch);
       }
-      const bool need_exact = !a.stale || k == 1 || (__ldcg(a.guard) == k);
+      const bool need_exact = !fused || (__ldcg(a.guard) == k);
       if (need_exact) {
-        if (threadIdx.x == 0 && b == 0 && a.stale && k > 1) atomicAdd(a.stats + 1, 1);
-#pragma unroll
-        for (int e = 0; e < E; ++e) { acc[e] = -INFINITY; gsl[e] = 0.f; }
-        run_pass<kPassColExact>(fb(k & 1), nullptr, false, false, err_dummy, bad, cost_dummy);
-        store_partials(true);
+        if (threadIdx.x == 0 && b == 0 && fused) atomicAdd(a.stats + 1, 1);
+        col_exact_pass(fb(k & 1));
         grid_barrier(a.bar, epoch);
         combine_pairs(gb(k & 1));
         grid_barrier(a.bar, epoch);
@@ -577,25 +710,19 @@ struct DenseSolver {
     if (!stopped) {
       // the final check at the cap (solver.py:286-316: in-loop if K % c == 0, else the extra one)
       final_k = a.max_iter;
-      load_columns(gb(final_k & 1));
-      float err_acc = 0.f, cost_dummy = 0.f;
-      int bad = 0;
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (!isfinite(gcol[e]) && col(e / 4, e % 4) < a.m) bad = 1;
-      run_pass<kPassCheck>(fb(final_k & 1), nullptr, false, true, err_acc, bad, cost_dummy);
-      bad = __syncthreads_or(bad);
-      if (threadIdx.x == 0) { a.errpart[b] = err_acc; a.flagpart[b] = bad; }
+      const bool gbad = load_columns(gb(final_k & 1));
+      float err_acc = 0.f;
+      int bad = gbad ? 1 : 0;
+      check_pass(fb(final_k & 1), err_acc, bad);
+      publish_check(err_acc, bad);
       grid_barrier(a.bar, epoch);
-      float e;
-      decide(final_k, failed, e);
+      decide(final_k, failed);
     }
     const int fbuf = final_k & 1;
     if (!failed && a.want_cost) {
       load_columns(gb(fbuf));
-      float err_acc = 0.f, cost_acc = 0.f;
-      int bad = 0;
-      run_pass<kPassCost>(fb(fbuf), nullptr, false, false, err_acc, bad, cost_acc);
+      float cost_acc = 0.f;
+      cost_pass(fb(fbuf), cost_acc);
       if (threadIdx.x == 0) a.costpart[b] = cost_acc;
       grid_barrier(a.bar, epoch);
       if (b == 0) {

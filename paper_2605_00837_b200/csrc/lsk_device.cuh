@@ -213,3 +213,65 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch)
 }
 
 }  // namespace lsk
+
+namespace lsk {
+// ---- packed fp32 pairs (sm_100a add/sub/mul/fma.rn.f32x2 -> FADD2/FMUL2/FFMA2).
+// Each lane of a packed op is ONE IEEE round-to-nearest op, so the reference's
+// separately rounded argument build is preserved bit for bit while the FMA
+// pipe issue count halves (profiles/r1_v1_dense_ncu.md).
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk2(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void up2(f2 v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 ex2x2(f2 t) {
+  float a, b;
+  up2(t, a, b);
+  return pk2(ex2(a), ex2(b));
+}
+// two packed pairs (4 consecutive floats) from shared memory
+__device__ __forceinline__ void lds2x2(const float* p, f2& lo, f2& hi) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(smem_u32(p)));
+}
+// fl(fl(u * s) + l) lane-wise with the add done as two scalar FADDs: ptxas
+// contracts a packed mul.rn.f32x2 feeding add.rn.f32x2 into one FFMA2 even
+// with -fmad=false (the .rn qualifiers do not stop it on f32x2), which would
+// break the reference's separately rounded argument build.
+// tests/test_abi.py checks the SASS for contracted argument builds.
+__device__ __forceinline__ f2 muladd_rn2(f2 u, f2 s, f2 l) {
+  float u0, u1, l0, l1;
+  up2(mul2(u, s), u0, u1);
+  up2(l, l0, l1);
+  return pk2(__fadd_rn(u0, l0), __fadd_rn(u1, l1));
+}
+// reference argument fl(fl(fl(a - c) * s) + l), lane-wise
+__device__ __forceinline__ f2 arg3x2(f2 a, f2 c, f2 s, f2 l) { return muladd_rn2(sub2(a, c), s, l); }
+// check argument fl(fl(fl(fl(f + g) - c) * s) + l), lane-wise
+__device__ __forceinline__ f2 arg4x2(f2 f, f2 g, f2 c, f2 s, f2 l) {
+  return muladd_rn2(sub2(add2(f, g), c), s, l);
+}
+}  // namespace lsk
