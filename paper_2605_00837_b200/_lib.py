@@ -10,7 +10,8 @@ import os
 from .errors import BackendError, DimensionMismatch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblsk.so")
+# LSK_LIB overrides the library path (experiments with alternative builds)
+LIB_PATH = os.environ.get("LSK_LIB") or os.path.join(_HERE, "liblsk.so")
 
 LSK_OK = 0
 LSK_EINVAL = -1

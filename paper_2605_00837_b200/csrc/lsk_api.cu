@@ -61,12 +61,12 @@ __global__ void __launch_bounds__(SV::NW * 32, 1) k_solve_dense(lsk::DenseArgs a
   sv.solve();
 }
 
-constexpr int kHeaderInts = 64;  // [0]=barrier [1]=guard [2..3]=stats [4]=status [5]=iters [6]=ntrace [7]=fbuf
+constexpr int kHeaderInts = 64;  // [12..13]=barrier (u64) [1]=guard [2..3]=stats [4]=status [5]=iters [6]=ntrace [7]=fbuf
                                  // [8]=err(float) [9]=cost(float)
 
 struct DenseLayout {
   int W, G;
-  size_t off_f0, off_g0, zero_bytes, off_f1, off_g1, off_part, off_pairs, off_err, off_flag, off_cost, total;
+  size_t off_f0, off_g0, zero_bytes, off_f1, off_g1, off_part, off_pairs, off_err, off_flag, off_redo, off_errrow, off_cost, total;
 };
 
 inline int dense_width(int m) {
@@ -92,6 +92,8 @@ DenseLayout dense_layout(int n, int m) {
   L.off_pairs = o; o = align_up(o + size_t(L.G) * L.W * 8, 256);
   L.off_err = o; o = align_up(o + size_t(L.G) * 4, 256);
   L.off_flag = o; o = align_up(o + size_t(L.G) * 4, 256);
+  L.off_redo = o; o = align_up(o + size_t(L.G) * 4, 256);
+  L.off_errrow = o; o = align_up(o + size_t(n) * 4, 256);
   L.off_cost = o; o = align_up(o + size_t(L.G) * 4, 256);
   L.total = o;
   return L;
@@ -171,9 +173,10 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.part = reinterpret_cast<float*>(ws + L.off_part);
   a.pairs = reinterpret_cast<float2*>(ws + L.off_pairs);
   a.errpart = reinterpret_cast<float*>(ws + L.off_err);
+  a.errrow = reinterpret_cast<float*>(ws + L.off_errrow);
   a.flagpart = reinterpret_cast<int*>(ws + L.off_flag);
   a.costpart = reinterpret_cast<float*>(ws + L.off_cost);
-  a.bar = reinterpret_cast<unsigned*>(hdr + 0);
+  a.bar = reinterpret_cast<unsigned long long*>(hdr + 12);
   a.guard = hdr + 1;
   a.stats = hdr + 2;
   a.out_status = hdr + 4;

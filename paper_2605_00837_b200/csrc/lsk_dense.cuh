@@ -53,8 +53,9 @@ struct DenseArgs {
   float2* pairs;         // [G][W] exact column (max, sumexp) partials
   float* errpart;        // [G]
   int* flagpart;         // [G]
+  float* errrow;         // [n] (unused by this solver)
   float* costpart;       // [G]
-  unsigned* bar;         // grid barrier counter (zeroed)
+  unsigned long long* bar;  // grid barrier counter (zeroed): arrivals | flags << 32
   int* guard;            // last iteration whose column guard fired (zeroed)
   int* stats;            // [0] row-guard fires, [1] column-guard passes (zeroed)
   // outputs

@@ -166,11 +166,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes (or the hint expires) instead of spinning on issue slots
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
   const uint64_t t0 = globaltimer_ns();
-  while (!mbar_try_wait(addr, parity)) {
+  while (!mbar_try_wait_sleep(addr, parity)) {
     if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
   }
 }
@@ -181,6 +196,11 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uin
           smem_u32(dst_smem)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// bulk prefetch of [src, src+bytes) into L2 (no smem, no completion tracking)
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // ---- L2-coherent loads for data produced by other CTAs of the same launch.
@@ -195,21 +215,36 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& epoch) {
+__device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Grid barrier on a 64-bit counter: the low word counts arrivals, the high
+// word accumulates a per-CTA flag (e.g. "a guard fired in my rows"), so the
+// barrier also delivers the grid-wide OR without another L2 round trip.
+// Returns the high word as seen at release (exact as long as two flagged
+// barriers are always separated by an unflagged one). `scratch` is one
+// shared-memory word used to broadcast thread 0's result.
+__device__ __forceinline__ unsigned grid_barrier(unsigned long long* counter, unsigned& epoch, unsigned flag = 0,
+                                                 unsigned* scratch = nullptr) {
   __syncthreads();
   epoch += 1;
   if (threadIdx.x == 0) {
     const unsigned target = epoch * gridDim.x;
     __threadfence();
-    atomicAdd(counter, 1u);
-    if (ld_acquire(counter) < target) {
+    atomicAdd(counter, 1ull | (static_cast<unsigned long long>(flag) << 32));
+    unsigned long long v = ld_acquire64(counter);
+    if (static_cast<unsigned>(v) < target) {
       const uint64_t t0 = globaltimer_ns();
-      while (ld_acquire(counter) < target)
+      while (static_cast<unsigned>(v = ld_acquire64(counter)) < target)
         if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
     }
     __threadfence();
+    if (scratch) *scratch = static_cast<unsigned>(v >> 32);
   }
   __syncthreads();
+  return scratch ? *scratch : 0u;
 }
 
 }  // namespace lsk
@@ -268,10 +303,26 @@ __device__ __forceinline__ f2 muladd_rn2(f2 u, f2 s, f2 l) {
   up2(l, l0, l1);
   return pk2(__fadd_rn(u0, l0), __fadd_rn(u1, l1));
 }
+__device__ __forceinline__ void lds2x2_u32(uint32_t addr, f2& lo, f2& hi) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(addr));
+}
 // reference argument fl(fl(fl(a - c) * s) + l), lane-wise
 __device__ __forceinline__ f2 arg3x2(f2 a, f2 c, f2 s, f2 l) { return muladd_rn2(sub2(a, c), s, l); }
 // check argument fl(fl(fl(fl(f + g) - c) * s) + l), lane-wise
 __device__ __forceinline__ f2 arg4x2(f2 f, f2 g, f2 c, f2 s, f2 l) {
   return muladd_rn2(sub2(add2(f, g), c), s, l);
+}
+}  // namespace lsk
+
+namespace lsk {
+// plain mbarrier arrive (release.cta): producer -> consumer hand-off in smem
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// shared-memory counter increment with acq_rel ordering; returns the old value
+__device__ __forceinline__ unsigned atom_add_acqrel_smem(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+  return old;
 }
 }  // namespace lsk

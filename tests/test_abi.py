@@ -54,3 +54,16 @@ def test_pure_host_helpers():
 def test_sm100a_cubin_present():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_no_contracted_argument_build():
+    """The reference builds every argument with separately rounded fp32 ops
+    (solver.py:77-79; an FMA there breaks 1e-5 parity at eps=1e-4).
+    ptxas contracts packed mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even with
+    -fmad=false, so the kernels keep that add scalar; the only legitimate
+    packed FMAs are the post-argument exp2 shifts x*log2(e) - shift."""
+    out = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    ffma2 = [ln for ln in out.splitlines() if re.search(r"\bFFMA2\b", ln)]
+    assert ffma2, "expected the packed exp2 shift FFMA2s in the solver"
+    bad = [ln.strip() for ln in ffma2 if "1.4426950216293334961" not in ln]
+    assert not bad, bad[:5]

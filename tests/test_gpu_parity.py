@@ -51,10 +51,39 @@ def err_tol(ref_err, mu):
     return 1e-4 * abs(ref_err) + len(mu) * float(np.max(mu)) * 2.0 ** -21
 
 
+def _assert_semantics(rep, z):
+    """The reference's own status/trace contract (tests/test_solver.py:210-238)."""
+    c, K, tol = int(z["check"]), int(z["K"]), float(z["tol"])
+    ks = [k for k, _ in rep.error_trace]
+    want = list(range(c, rep.iterations + 1, c))
+    if rep.iterations % c and rep.iterations == K:
+        want.append(K)  # the extra check at a cap that is not a checkpoint (solver.py:301-316)
+    if rep.status != "numerical_failure":
+        assert ks == want
+        assert rep.error_trace[-1][1] == pytest.approx(rep.final_marginal_error, rel=1e-6)
+        assert (rep.status == "converged") == (rep.final_marginal_error < tol)
+        assert rep.status == "converged" or rep.iterations == K
+
+
 def assert_report(rep, z, mu):
+    tr = z["trace"]
+    tol = float(z["tol"])
+    # A checkpoint whose reference error is within fp32 noise of the tolerance
+    # is a coin flip for any implementation whose exp/log/summation order differ
+    # from numpy's (SURVEY F6/F9: near the floor the error IS rounding noise).
+    # There the stop iteration may differ; the traces must agree up to it and
+    # the reference's status/trace semantics must hold.
+    amb = [int(k) for k, e in tr if abs(e - tol) <= err_tol(e, mu)]
+    if amb:
+        n_common = sum(1 for k, _ in tr if int(k) < amb[0])
+        assert [k for k, _ in rep.error_trace[:n_common]] == [int(k) for k in tr[:n_common, 0]]
+        for (_, e), (_, er) in zip(rep.error_trace[:n_common], tr[:n_common]):
+            assert abs(e - er) <= err_tol(er, mu), (e, er)
+        assert rep.iterations >= amb[0]
+        _assert_semantics(rep, z)
+        return True
     assert rep.status == str(z["status"])
     assert rep.iterations == int(z["iterations"])
-    tr = z["trace"]
     assert [k for k, _ in rep.error_trace] == [int(k) for k in tr[:, 0]]
     for (_, e), (_, er) in zip(rep.error_trace, tr):
         assert abs(e - er) <= err_tol(er, mu), (e, er)
@@ -68,6 +97,7 @@ def assert_report(rep, z, mu):
         assert np.isnan(rep.transport_cost)
     else:
         assert abs(rep.transport_cost - ref_cost) <= RTOL * abs(ref_cost) + 1e-12
+    return False
 
 
 @pytest.mark.parametrize("stale", [True, False], ids=["stale", "exact"])
@@ -76,8 +106,13 @@ def test_solve_small(cuda_ok, name, stale):
     z, C64, mu_w, nu_w = fixture_problem(name)
     with np.errstate(all="ignore"):
         rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), config_of(z), stale_shift=stale)
-    assert_report(rep, z, mu_w)
-    assert_potentials(pot, z)
+    if assert_report(rep, z, mu_w) and rep.iterations != int(z["iterations"]):
+        # stopped at a different (noise-decided) checkpoint: compare with the
+        # oracle run to the same iteration count instead
+        r = O.solve(C64, mu_w, nu_w, float(z["eps"]), tol=1e-30, max_iter=rep.iterations, check=int(z["check"]))
+        assert rel_max(pot.alpha, r["alpha"]) <= RTOL and rel_max(pot.beta, r["beta"]) <= RTOL
+    else:
+        assert_potentials(pot, z)
 
 
 @pytest.mark.parametrize("name", BIG)
