@@ -128,6 +128,48 @@ int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t 
 int32_t lsk_cast_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int32_t n, int32_t m, float* dst,
                           int64_t ldd, void* stream);
 
+
+/* ---------------------------------------------------------------------------
+ * On-the-fly point-cloud solver (configs C4/C5): the squared-Euclidean cost is
+ * recomputed in registers from fp32 points and never stored.
+ *
+ * Replaces the composition squared_euclidean_cost(X, Y) [/ C.max()] -> solve
+ * (costs.py:36-50, applications.py:177-191 / estimator.py:78-99,
+ * solver.py:230-337) for B independent problems of the same shape:
+ * X (B, n, d) and Y (B, m, d) fp64 (rounded once to fp32 on the device),
+ * d in 1..3; cost c_ij = scale[b] * sum_k (x_ik - y_jk)^2 with scale (B floats,
+ * device) = 1 or 1/Cmax (lsk_points_cost_max). log_mu/mu (B, n), log_nu (B, m)
+ * fp32 device. Same iteration, check, trace and status semantics as
+ * lsk_solve_dense_f32, per problem; a problem that stops no longer runs.
+ * Outputs: f_out (B, n), g_out (B, m), trace_iter/trace_err (B, capacity),
+ * result (B, 8) int32 (LSK_RES_*), result_f (B, 2) float (final error, cost).
+ * comm: NULL, or an lsk_comm_create() communicator of P ranks (B must be 1,
+ * P must divide n and m): rank r owns rows [r n/P, (r+1) n/P) for the f update
+ * and columns [r m/P, (r+1) m/P) for the g update; potentials are allgathered
+ * after each half-step, so results are bit-identical to one GPU for any P.
+ * Numerics: fp32 direct-form cost (~2-3e-6 on potentials at
+ * eps = 1e-3); use the dense path with lsk_build_cost_f32 below eps = 1e-3.
+ */
+size_t lsk_solve_points_workspace_bytes(int32_t B, int32_t n, int32_t m);
+int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
+                             const float* scale, const float* log_mu, const float* log_nu, const float* mu,
+                             double eps, double tol, int32_t max_iter, int32_t check_interval, int32_t flags,
+                             float* f_out, float* g_out, int32_t* trace_iter, float* trace_err, int32_t* result,
+                             float* result_f, void* workspace, size_t workspace_bytes, void* comm, void* stream);
+
+/* cmax_out[b] = max_ij sum_k (x_ik - y_jk)^2 in fp64 (device doubles), the
+ * C.max() normaliser of applications.py:186-188, without materialising C. */
+int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
+                            double* cmax_out, void* stream);
+
+/* NCCL communicator for the sharded points solve (one rank per GPU): rank 0
+ * gets an id (lsk_nccl_unique_id_bytes() bytes), every rank passes it to
+ * lsk_comm_create with its own device current. */
+int32_t lsk_nccl_unique_id_bytes(void);
+int32_t lsk_nccl_unique_id(void* id_out);
+int32_t lsk_comm_create(const void* id, int32_t nranks, int32_t rank, void** comm_out);
+int32_t lsk_comm_destroy(void* comm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,23 @@ BUILD = os.path.join(ROOT, "build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
-UNITS = ["lsk_api.cu"]
+UNITS = ["lsk_api.cu", "lsk_points.cu"]
+
+
+def nccl_dirs():
+    """NCCL headers/library: the copy bundled with torch (2.28, the one torch
+    itself loads), else the system one."""
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+        if spec and spec.submodule_search_locations:
+            root = list(spec.submodule_search_locations)[0]
+            if os.path.exists(os.path.join(root, "include", "nccl.h")):
+                return os.path.join(root, "include"), os.path.join(root, "lib")
+    except Exception:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
 def nvcc():
@@ -46,14 +62,17 @@ def build(verbose=False, force=False):
     objs = []
     for u in UNITS:
         obj = os.path.join(BUILD, u.replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", os.path.join(CSRC, u), "-o", obj]
+        inc, _ = nccl_dirs()
+        cmd = [nvcc(), *ARCH, *FLAGS, "-I" + inc, "-c", os.path.join(CSRC, u), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcuda"]
+    _, libdir = nccl_dirs()
+    nccl = os.path.join(libdir, "libnccl.so.2")
+    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcuda", "-Xlinker", nccl, "-Xlinker", "-rpath=" + libdir]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

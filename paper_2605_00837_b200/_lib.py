@@ -44,6 +44,15 @@ SIGNATURES = {
     "lsk_build_cost_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p,
                                     _c_sz, _c_p]),
     "lsk_cast_cost_f32": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_p]),
+    "lsk_solve_points_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
+    "lsk_solve_points_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl,
+                                      _c_dbl, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                      _c_sz, _c_p, _c_p]),
+    "lsk_points_cost_max": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p]),
+    "lsk_nccl_unique_id_bytes": (_c_i32, []),
+    "lsk_nccl_unique_id": (_c_i32, [_c_p]),
+    "lsk_comm_create": (_c_i32, [_c_p, _c_i32, _c_i32, _c_p]),
+    "lsk_comm_destroy": (_c_i32, [_c_p]),
 }
 
 _lib = None

@@ -125,6 +125,10 @@ int32_t check_dense(const float* C, int64_t ldc, int32_t n, int32_t m) {
 
 }  // namespace
 
+namespace lsk_host {
+int32_t fail(int32_t code, const std::string& msg) { return ::fail(code, msg); }
+}  // namespace lsk_host
+
 extern "C" {
 
 const char* lsk_last_error(void) { return g_err.c_str(); }

@@ -1,0 +1,371 @@
+// On-the-fly squared-Euclidean log-domain Sinkhorn kernels (configs C4/C5):
+// the cost c_ij = scale * sum_k (x_ik - y_jk)^2 is recomputed in registers
+// from fp32 point clouds and never stored (C4 at n=m=65536 would be 17 GB).
+//
+// Reference path replaced: squared_euclidean_cost (costs.py:36-50) [+ C/C.max()
+// of applications.py:186-188] followed by solve (solver.py:230-337). Because
+// the cost is symmetric in the roles of the two clouds, the g-update is the
+// f-update with (X, f, log mu) and (Y, g, log nu) swapped: one
+// "row LSE over points" kernel serves both half-steps.
+//
+// One half-step (rows R with old potential p_i, columns Q with potential q_j
+// and log-weights l_j):
+//   p_i^new = neg_eps * LSE_j( (q_j - c_ij) * inv_eps + l_j )
+// computed in log2 units as
+//   v_ij = A_j - K * (sum_k d_k^2 + init_i),  A_j = (q_j * inv_eps + l_j) * log2 e,
+//   K = inv_eps * log2 e * scale,  init_i = -p_i / scale  (stale shift)
+// so v_ij = log2(e) * (x_ij - sh_i) with sh_i = -p_i * inv_eps; the row shift is
+// folded into the start value of the coordinate sum (no extra op per pair).
+// Per pair: 3 sub + 3 fma (cost) + 1 fma (argument) + 1 add, packed two rows
+// per f32x2 op, and one MUFU ex2: the FP32 lanes and the MUFU pipe are
+// balanced at 16 pairs/clk/SM.
+//
+// Numerics: the cost is fp32 from fp32-rounded points in the direct form (the
+// reference builds it in fp64 and rounds once); SURVEY F5 measures this at
+// 2-3e-6 on the potentials at eps=1e-3, inside the 1e-5 bar. Use the dense
+// solver (fp32(C64) bit for bit) for eps < 1e-3.
+#pragma once
+#include "lsk_device.cuh"
+
+namespace lsk {
+
+constexpr int kPtsThreads = 256;            // 8 warps
+constexpr int kPtsRowsPerWarp = 8;          // 4 packed row pairs per lane
+constexpr int kPtsTileRows = 8 * kPtsRowsPerWarp;  // 64 rows per CTA tile
+constexpr int kPtsChunk = 2048;             // columns per chunk (32 KB of smem)
+
+enum PtsMode { kPtsStale = 0, kPtsOnline = 1, kPtsCost = 2 };
+
+struct PtsHalf {
+  // problem b's rows/cols: rows_b = rows + b * n_rows, etc.
+  int B, n_rows, n_cols;
+  int row_lo, row_hi;          // this rank's slab of rows [row_lo, row_hi)
+  int chunks;                  // ceil(n_cols / kPtsChunk)
+  const float4* rpts;          // (B, n_rows) points (x, y, z, 0)
+  const float4* cpts;          // (B, n_cols)
+  const float* rpot;           // (B, n_rows) old row potential (stale shift / cost)
+  const float* cpot;           // (B, n_cols) column potential
+  const float* clw;            // (B, n_cols) column log-weights
+  const float* rlw;            // (B, n_rows) row log-weights (cost mode)
+  const float* scale;          // (B) cost scale (1/Cmax or 1)
+  float inv_eps;
+  void* part;                  // (B, chunks, n_rows) float (stale/cost) or float2 (online)
+  const int* active;           // (B) problem still iterating (nullptr = all)
+  const int* rowflag;          // (B, n_rows) online mode: only rows flagged here
+  const int* nflag;            // online mode: number of flagged rows (0 -> exit)
+};
+
+__device__ __forceinline__ f2 bc2(float a) { return pk2(a, a); }
+
+// One CTA = one (problem, 64-row tile of the slab, column chunk) unit.
+template <int MODE>
+__global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
+  __shared__ __align__(16) float4 colv[kPtsChunk];
+  __shared__ int tile_any;
+  const int ch = blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
+  if (MODE == kPtsOnline && h.nflag && *h.nflag == 0) return;
+  if (h.active && !h.active[b]) return;
+  const int r_base = h.row_lo + tile * kPtsTileRows;
+  if (r_base >= h.row_hi) return;
+  if (MODE == kPtsOnline && h.rowflag) {
+    if (threadIdx.x == 0) tile_any = 0;
+    __syncthreads();
+    if (threadIdx.x < kPtsTileRows) {
+      const int r = r_base + threadIdx.x;
+      if (r < h.row_hi && h.rowflag[(size_t)b * h.n_rows + r]) tile_any = 1;
+    }
+    __syncthreads();
+    if (!tile_any) return;
+  }
+  const float sc = __ldg(h.scale + b);
+  const float l2 = kLog2e;
+  const int j0 = ch * kPtsChunk;
+  const int ncol = min(kPtsChunk, h.n_cols - j0);
+  // stage the chunk: (y0, y1, y2, A_j), A_j = (q_j * inv + l_j) * log2e
+  for (int t = threadIdx.x; t < ncol; t += kPtsThreads) {
+    const size_t j = (size_t)b * h.n_cols + j0 + t;
+    float4 q = __ldg(h.cpts + j);
+    const float A = __fmul_rn(__fmaf_rn(__ldg(h.cpot + j), h.inv_eps, __ldg(h.clw + j)), l2);
+    q.w = A;
+    colv[t] = q;
+  }
+  // this warp's 8 rows, packed in pairs
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  f2 X0[4], X1[4], X2[4], I0[4];
+  float lrow[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    float xa[3], xb[3], ia, ib;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      int r = r_base + w * kPtsRowsPerWarp + 2 * p + h2;
+      r = r < h.row_hi ? r : h.row_hi - 1;
+      const size_t ri = (size_t)b * h.n_rows + r;
+      const float4 x = __ldg(h.rpts + ri);
+      float init = 0.f;
+      if (MODE != kPtsOnline) init = __fdiv_rn(-__ldg(h.rpot + ri), sc);
+      if (MODE == kPtsCost) lrow[2 * p + h2] = __ldg(h.rlw + ri);
+      if (h2 == 0) { xa[0] = x.x; xa[1] = x.y; xa[2] = x.z; ia = init; }
+      else { xb[0] = x.x; xb[1] = x.y; xb[2] = x.z; ib = init; }
+    }
+    X0[p] = pk2(xa[0], xb[0]);
+    X1[p] = pk2(xa[1], xb[1]);
+    X2[p] = pk2(xa[2], xb[2]);
+    I0[p] = pk2(ia, ib);
+  }
+  const float Kf = __fmul_rn(__fmul_rn(h.inv_eps, l2), sc);
+  const f2 NK = bc2(-Kf);
+  __syncthreads();
+
+  f2 acc[4];
+  float mx[8], sm[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) acc[p] = 0ull;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) { mx[r] = -INFINITY; sm[r] = 0.f; }
+
+#pragma unroll 2
+  for (int t = lane; t < ncol; t += 32) {
+    const float4 q = colv[t];
+    const f2 Q0 = bc2(q.x), Q1 = bc2(q.y), Q2 = bc2(q.z), QA = bc2(q.w);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      f2 d = sub2(X0[p], Q0);
+      f2 s = (MODE == kPtsCost) ? mul2(d, d) : fma2(d, d, I0[p]);
+      d = sub2(X1[p], Q1);
+      s = fma2(d, d, s);
+      d = sub2(X2[p], Q2);
+      s = fma2(d, d, s);
+      if (MODE == kPtsStale) {
+        acc[p] = add2(acc[p], ex2x2(fma2(s, NK, QA)));
+      } else if (MODE == kPtsCost) {
+        // c_ij * exp(z_ij), z = ((f_i + g_j) - c_ij) * inv + lmu_i + lnu_j
+        const f2 v = fma2(add2(s, I0[p]), NK, QA);
+        float v0, v1, s0, s1;
+        up2(v, v0, v1);
+        up2(s, s0, s1);
+        const float e0 = ex2(__fmaf_rn(lrow[2 * p], l2, v0)), e1 = ex2(__fmaf_rn(lrow[2 * p + 1], l2, v1));
+        acc[p] = add2(acc[p], pk2(__fmul_rn(__fmul_rn(s0, sc), e0), __fmul_rn(__fmul_rn(s1, sc), e1)));
+      } else {  // online (max, sum) in log2 units
+        float v0, v1;
+        up2(fma2(s, NK, QA), v0, v1);
+        const float vv[2] = {v0, v1};
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int r = 2 * p + h2;
+          const float mn = fmax_nan(mx[r], vv[h2]);
+          const float ms = (fabsf(mn) <= 3.402823466e38f) ? mn : 0.f;
+          sm[r] = __fmaf_rn(sm[r], (mx[r] == -INFINITY) ? 0.f : ex2(mx[r] - ms), ex2(vv[h2] - ms));
+          mx[r] = mn;
+        }
+      }
+    }
+  }
+  // lane reduction (xor butterfly: fixed order) and store
+  const size_t pbase = ((size_t)b * h.chunks + ch) * h.n_rows;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int r8 = 2 * p + h2;
+      const int r = r_base + w * kPtsRowsPerWarp + r8;
+      if (MODE != kPtsOnline) {
+        float a0, a1;
+        up2(acc[p], a0, a1);
+        const float v = warp_sum(h2 == 0 ? a0 : a1);
+        if (lane == 0 && r < h.row_hi) reinterpret_cast<float*>(h.part)[pbase + r] = v;
+      } else {
+        float m2 = mx[r8], s2 = sm[r8];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const float mo = __shfl_xor_sync(0xffffffffu, m2, o), so = __shfl_xor_sync(0xffffffffu, s2, o);
+          // merge in log2 units
+          const float mm = fmax_nan(m2, mo);
+          const float mms = (fabsf(mm) <= 3.402823466e38f) ? mm : 0.f;
+          const float wa = (m2 == -INFINITY) ? 0.f : ex2(m2 - mms), wb = (mo == -INFINITY) ? 0.f : ex2(mo - mms);
+          s2 = __fmaf_rn(s2, wa, so * wb);
+          m2 = mm;
+        }
+        if (lane == 0 && r < h.row_hi) reinterpret_cast<float2*>(h.part)[pbase + r] = make_float2(m2, s2);
+      }
+    }
+  }
+}
+
+struct PtsCombine {
+  int B, n_rows, row_lo, row_hi, chunks;
+  const void* part;
+  const float* rpot_old;  // (B, n_rows) stale potential (shift); for check: f^k
+  float* rpot_new;        // (B, n_rows) new potential (nullptr: check only)
+  float inv_eps, neg_eps;
+  const int* active;
+  int* rowflag;           // stale: set rows whose sum left the guard band
+  int* nflag;             // stale: count of such rows
+  // check (f-update only): per-row error terms of iterate k
+  const float* rlw;       // log mu
+  const float* rmu;       // mu
+  const float* cpot;      // g^k (finiteness)
+  float* errrow;          // (B, n_rows)
+  int* badrow;            // (B) a non-finite f^k or g^k was seen
+  int check;
+  const int* nflag_in;    // online: number of flagged rows (0 -> exit)
+};
+
+// per (problem, row): combine the chunk partials in fixed order
+template <int MODE>
+__global__ void k_pts_combine(PtsCombine c) {
+  const int b = blockIdx.y;
+  const int r = c.row_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (MODE == kPtsOnline && c.nflag_in && *c.nflag_in == 0) return;
+  if (r >= c.row_hi) return;
+  if (c.active && !c.active[b]) return;
+  const size_t ri = (size_t)b * c.n_rows + r;
+  if (MODE == kPtsOnline) {
+    if (c.rowflag && !c.rowflag[ri]) return;
+    const float2* p = reinterpret_cast<const float2*>(c.part);
+    float m2 = -INFINITY, s2 = 0.f;
+    for (int ch = 0; ch < c.chunks; ++ch) {
+      const float2 v = p[((size_t)b * c.chunks + ch) * c.n_rows + r];
+      const float mm = fmax_nan(m2, v.x);
+      const float mms = (fabsf(mm) <= 3.402823466e38f) ? mm : 0.f;
+      const float wa = (m2 == -INFINITY) ? 0.f : ex2(m2 - mms), wb = (v.x == -INFINITY) ? 0.f : ex2(v.x - mms);
+      s2 = __fmaf_rn(s2, wa, v.y * wb);
+      m2 = mm;
+    }
+    // LSE = M2 * ln2 + ln S (reduction.py:196-207: an all -inf row gives -inf)
+    float L;
+    if (!(fabsf(m2) <= 3.402823466e38f)) L = -INFINITY;
+    else L = __fadd_rn(__fmul_rn(m2, 0.6931471805599453f), logf(fmaxf(s2, kSumFloor)));
+    if (c.rpot_new) c.rpot_new[ri] = __fmul_rn(c.neg_eps, L);
+    if (c.rowflag) c.rowflag[ri] = 0;
+    return;
+  }
+  const float* p = reinterpret_cast<const float*>(c.part);
+  float S = 0.f;
+  for (int ch = 0; ch < c.chunks; ++ch) S += p[((size_t)b * c.chunks + ch) * c.n_rows + r];
+  const float pold = c.rpot_old[ri];
+  const float sh = __fmul_rn(-pold, c.inv_eps);
+  const bool ok = S >= kShiftLo && S <= kShiftHi;
+  if (c.rpot_new) {
+    c.rpot_new[ri] = __fmul_rn(c.neg_eps, lse_finish(sh, S));
+    if (!ok) {
+      c.rowflag[ri] = 1;
+      atomicAdd(c.nflag, 1);
+    }
+  }
+  if (c.check) {
+    // the stale sum with shift -f^k * inv is exactly the check sum of iterate k:
+    // r_i = exp(log mu_i + LSE_j(((f_i + g_j) - c_ij) * inv + log nu_j)) (solver.py:97-104)
+    const float rr = expf(__fadd_rn(c.rlw[ri], logf(fmaxf(S, kSumFloor))));
+    c.errrow[ri] = fabsf(__fsub_rn(rr, c.rmu[ri]));
+    if (!isfinite(pold) || !ok) {
+      if (!isfinite(pold)) atomicOr(c.badrow + b, 1);
+    }
+  }
+}
+
+// non-finite g^k (columns) for the check's finiteness test (solver.py:287-290)
+__global__ void k_pts_colcheck(int B, int n, const float* __restrict__ pot, const int* active, int* bad) {
+  const int b = blockIdx.y;
+  if (active && !active[b]) return;
+  int any = 0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    any |= !isfinite(pot[(size_t)b * n + j]);
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(bad + b, 1);
+}
+
+// Per (problem, block of kPtsBlk rows): fixed-order sums of per-row terms.
+// The block size is independent of the number of ranks, so a sharded solve
+// sums exactly the same blocks in the same order as a single GPU.
+constexpr int kPtsBlk = 1024;
+__global__ void __launch_bounds__(1024) k_pts_blocksum(int B, int n, int lo, int hi, const float* __restrict__ v,
+                                                        const int* active, float* __restrict__ blk) {
+  __shared__ float red[64];
+  const int b = blockIdx.y, k = blockIdx.x;
+  const int r0 = lo + k * kPtsBlk;
+  if (r0 >= hi) return;
+  if (active && !active[b]) return;
+  float s[1] = {0.f};
+  const int r = r0 + threadIdx.x;
+  if (r < hi) s[0] = v[(size_t)b * n + r];
+  block_reduce<1024, 1, false>(s, red);
+  if (threadIdx.x == 0) blk[(size_t)b * ((n + kPtsBlk - 1) / kPtsBlk) + (r0 / kPtsBlk)] = s[0];
+}
+
+// Per-problem state for the batched solve (all device-resident).
+struct PtsState {
+  int active;     // still iterating
+  int status;     // 0 not_converged, 1 converged, 2 numerical_failure
+  int iters;
+  int ntrace;
+  int fbuf;       // buffer holding the returned f (and g)
+  int pad[3];
+  float err;
+  float cost;
+};
+
+// check decision for every problem (solver.py:286-300): err = fixed-order sum
+// of the row-block sums; stop on non-finite f/g, non-finite err or err < tol.
+// kk = the iterate being checked; final = the check at the cap.
+__global__ void k_pts_decide(int B, int n, const float* __restrict__ blk, int* bad, double tol, int kk, int final,
+                             PtsState* st, int* trace_iter, float* trace_err, int cap) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  PtsState& s = st[b];
+  if (!s.active) return;
+  const int nb = (n + kPtsBlk - 1) / kPtsBlk;
+  float err = 0.f;
+  for (int k = 0; k < nb; ++k) err += blk[(size_t)b * nb + k];
+  const int isbad = bad[b];
+  bad[b] = 0;
+  int status = 0;
+  bool stop = false, append = true;
+  float e = err;
+  if (isbad) { stop = true; status = 2; e = NAN; append = false; }
+  else if (!isfinite(err)) { stop = true; status = 2; }
+  else if (err < tol) { stop = true; status = 1; }
+  if (append && s.ntrace < cap) {
+    trace_iter[(size_t)b * cap + s.ntrace] = kk;
+    trace_err[(size_t)b * cap + s.ntrace] = err;
+    s.ntrace += 1;
+  }
+  s.status = status;
+  s.err = e;
+  if (stop || final) {
+    s.active = 0;
+    s.iters = kk;
+    s.fbuf = kk & 1;
+  }
+}
+
+__global__ void k_pts_cost_finish(int B, int n, const float* __restrict__ blk, PtsState* st) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  PtsState& s = st[b];
+  if (s.status == 2) { s.cost = NAN; return; }
+  const int nb = (n + kPtsBlk - 1) / kPtsBlk;
+  float c = 0.f;
+  for (int k = 0; k < nb; ++k) c += blk[(size_t)b * nb + k];
+  if (!isfinite(c)) { s.status = 2; c = NAN; }
+  s.cost = c;
+}
+
+// fp64 points -> float4 (x, y, z, 0) with coordinates beyond d zero
+__global__ void k_pts_pack(const double* __restrict__ P, long long count, int d, float4* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+    float v[3] = {0.f, 0.f, 0.f};
+    for (int k = 0; k < d; ++k) v[k] = __double2float_rn(P[i * d + k]);
+    out[i] = make_float4(v[0], v[1], v[2], 0.f);
+  }
+}
+
+// select buffer s.fbuf into the outputs
+__global__ void k_pts_pick(int B, int n, const float* __restrict__ p0, const float* __restrict__ p1,
+                           const PtsState* st, float* __restrict__ out) {
+  const int b = blockIdx.y;
+  const float* src = st[b].fbuf ? p1 : p0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[(size_t)b * n + i] = src[(size_t)b * n + i];
+}
+
+}  // namespace lsk

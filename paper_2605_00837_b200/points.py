@@ -1,0 +1,160 @@
+"""Point-cloud solves with the cost recomputed on the fly (configs C4/C5).
+
+Drop-in for the reference composition ``squared_euclidean_cost(X, Y)``
+(``costs.py:36-50``), optionally ``C / C.max()`` (``applications.py:186-188``,
+``estimator.py:87-89``), then ``solve`` (``solver.py:230-337``) -- without ever
+materialising the (n, m) cost: one ``lsk_solve_points_f32`` call runs the whole
+solve for a batch of problems, recomputing ``sum_k (x_ik - y_jk)^2`` in
+registers. Returns the reference's ``(SolveReport, DualPotentials)``.
+
+* ``solve_points_otf``: one problem; with ``comm`` (``dist.Communicator``) the
+  rows and columns are sharded over the ranks (owner computes), bit-identical to
+  one GPU.
+* ``solve_points_batched``: B independent problems of one shape in a single
+  launch sequence; each problem stops on its own (per-problem status / trace).
+
+Numerics: fp32 cost from fp32-rounded points in the direct form (SURVEY F5:
+~2-3e-6 on the potentials at eps=1e-3). ``costs.solve_points`` picks this path
+automatically only where the fp64-exact dense matrix does not fit (m > 8192).
+"""
+
+import time
+
+import numpy as np
+
+from . import _lib
+from .costs import as_points
+from .errors import DimensionMismatch
+from .solver import _STATUS_BY_CODE, _ptr, _stream_ptr, _torch
+from .types import DualPotentials, SolveReport
+
+__all__ = ["solve_points_otf", "solve_points_batched", "points_cost_max"]
+
+
+def _batch_points(P):
+    """(B, k, d) float64 contiguous from a (k, d) / (B, k, d) array."""
+    A = np.asarray(P, dtype=np.float64)
+    if A.ndim == 2:
+        A = A[None]
+    if A.ndim != 3:
+        raise DimensionMismatch(f"point batch must be (B, k, d), got {A.shape}")
+    for b in range(A.shape[0]):
+        as_points(A[b])  # validation (EmptyInput / NonFiniteInput)
+    return np.ascontiguousarray(A)
+
+
+def _weights(dist, B, k, name):
+    """(B, k) fp64 weights and log-weights from None (uniform) / a
+    DiscreteDistribution / a sequence of them."""
+    if dist is None:
+        w = np.full((B, k), 1.0 / k)
+        return w, np.log(w)
+    if hasattr(dist, "weights"):
+        dist = [dist] * B
+    if len(dist) != B:
+        raise DimensionMismatch(f"{name}: expected {B} distributions, got {len(dist)}")
+    w = np.stack([np.asarray(d.weights, np.float64) for d in dist])
+    lw = np.stack([np.asarray(d.log_weights, np.float64) for d in dist])
+    if w.shape != (B, k):
+        raise DimensionMismatch(f"{name}: weights of shape {w.shape}, expected {(B, k)}")
+    return w, lw
+
+
+def points_cost_max(Xd, Yd):
+    """Exact fp64 max of the squared-Euclidean cost per problem (device)."""
+    torch = _torch()
+    B, n, d = Xd.shape
+    m = Yd.shape[1]
+    out = torch.empty(B, dtype=torch.float64, device="cuda")
+    _lib.call("lsk_points_cost_max", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(out), _stream_ptr(torch))
+    return out
+
+
+class _PointsRun:
+    __slots__ = ("B", "n", "m", "f", "g", "ti", "te", "res", "resf", "ev0", "ev1", "t0", "keep")
+
+
+def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm):
+    torch = _torch()
+    if config.precision != "single":
+        raise NotImplementedError("precision='double' is not available on the B200 path (fp32 only)")
+    if normalize not in ("none", "max"):
+        raise ValueError("normalize must be 'none' or 'max'")
+    Xb, Yb = _batch_points(X), _batch_points(Y)
+    if Xb.shape[0] != Yb.shape[0] or Xb.shape[2] != Yb.shape[2]:
+        raise DimensionMismatch(f"point batches {Xb.shape} and {Yb.shape} do not match")
+    B, n, d = Xb.shape
+    m = Yb.shape[1]
+    wmu, lmu = _weights(mu, B, n, "mu")
+    _, lnu = _weights(nu, B, m, "nu")
+    r = _PointsRun()
+    r.t0 = time.perf_counter()
+    r.B, r.n, r.m = B, n, m
+    Xd = torch.from_numpy(Xb).to("cuda")
+    Yd = torch.from_numpy(Yb).to("cuda")
+    if normalize == "max":
+        cmax = points_cost_max(Xd, Yd)
+        # reference: C / C.max() only when the cost has a non-zero range (applications.py:186-188)
+        scale = torch.where(cmax > 0, 1.0 / cmax, torch.ones_like(cmax)).to(torch.float32)
+    else:
+        scale = torch.ones(B, dtype=torch.float32, device="cuda")
+    lmu_d = torch.from_numpy(lmu.astype(np.float32)).to("cuda")
+    lnu_d = torch.from_numpy(lnu.astype(np.float32)).to("cuda")
+    mu_d = torch.from_numpy(wmu.astype(np.float32)).to("cuda")
+    K, c = int(config.max_iterations), int(config.check_interval)
+    cap = _lib.load().lsk_trace_capacity(K, c)
+    wsb = _lib.load().lsk_solve_points_workspace_bytes(B, n, m)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    r.f = torch.empty((B, n), dtype=torch.float32, device="cuda")
+    r.g = torch.empty((B, m), dtype=torch.float32, device="cuda")
+    r.ti = torch.zeros((B, cap), dtype=torch.int32, device="cuda")
+    r.te = torch.zeros((B, cap), dtype=torch.float32, device="cuda")
+    r.res = torch.zeros((B, 8), dtype=torch.int32, device="cuda")
+    r.resf = torch.zeros((B, 2), dtype=torch.float32, device="cuda")
+    flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
+    r.ev0 = torch.cuda.Event(enable_timing=True)
+    r.ev1 = torch.cuda.Event(enable_timing=True)
+    r.ev0.record()
+    _lib.call("lsk_solve_points_f32", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(scale), _ptr(lmu_d), _ptr(lnu_d),
+              _ptr(mu_d), float(config.epsilon), float(config.tolerance), K, c, flags, _ptr(r.f), _ptr(r.g),
+              _ptr(r.ti), _ptr(r.te), _ptr(r.res), _ptr(r.resf), _ptr(ws), wsb,
+              comm.handle if comm is not None else None, _stream_ptr(torch))
+    r.ev1.record()
+    r.keep = (Xd, Yd, scale, lmu_d, lnu_d, mu_d, ws)  # alive until the results are read
+    return r
+
+
+def _reports(r, return_device=False):
+    res = r.res.cpu().numpy()
+    resf = r.resf.cpu().numpy()
+    ti = r.ti.cpu().numpy()
+    te = r.te.cpu().numpy()
+    dev = r.ev0.elapsed_time(r.ev1) * 1e-3
+    f = r.f if return_device else r.f.cpu().numpy()
+    g = r.g if return_device else r.g.cpu().numpy()
+    elapsed = time.perf_counter() - r.t0
+    out = []
+    for b in range(r.B):
+        nt = int(res[b, 2])
+        status = _STATUS_BY_CODE[int(res[b, 0])]
+        rep = SolveReport(status=status, iterations=int(res[b, 1]), final_marginal_error=float(resf[b, 0]),
+                          transport_cost=float(resf[b, 1]) if status != "numerical_failure" else float("nan"),
+                          error_trace=tuple((int(k), float(e)) for k, e in zip(ti[b, :nt], te[b, :nt])),
+                          elapsed_seconds=elapsed, device_seconds=dev)
+        out.append((rep, DualPotentials(alpha=f[b], beta=g[b])))
+    return out
+
+
+def solve_points_otf(X, Y, mu, nu, config, normalize="none", *, stale_shift=True, comm=None, return_device=False):
+    """One on-the-fly solve of points X (n, d) vs Y (m, d); see module doc."""
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, comm)
+    return _reports(r, return_device)[0]
+
+
+def solve_points_batched(X, Y, config, mu=None, nu=None, normalize="none", *, stale_shift=True,
+                         return_device=False):
+    """B independent solves, X (B, n, d) vs Y (B, m, d), uniform marginals by
+    default (``mu``/``nu``: a DiscreteDistribution for all, or one per problem).
+    Returns a list of (SolveReport, DualPotentials)."""
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, None)
+    return _reports(r, return_device)

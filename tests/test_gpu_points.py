@@ -1,0 +1,98 @@
+"""On-the-fly points solver (configs C4/C5 shape) against the reference.
+
+The cost is fp32 from fp32-rounded points (never materialised), so parity is
+the north-star tolerance, not bit equality: potentials and transport cost
+within 1e-5 relative (max-norm) of the reference's single-precision solve at
+the same eps and iteration count (SURVEY F5 measures ~2-3e-6 at eps=1e-3).
+Fixtures: tests/golden/ (made by running the reference, make_golden.py).
+"""
+
+import numpy as np
+import pytest
+
+import lsk_oracle as O
+import paper_2605_00837_b200 as lsk
+from conftest import rel_max
+from inputs import fixture_points
+from paper_2605_00837_b200 import points as PT
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def dist(w):
+    w = np.asarray(w, np.float64)
+    return lsk.DiscreteDistribution(weights=w, log_weights=np.log(w))
+
+
+def config_of(z):
+    return lsk.SinkhornConfig(epsilon=float(z["eps"]), tolerance=float(z["tol"]),
+                              max_iterations=int(z["K"]), check_interval=int(z["check"]))
+
+
+@pytest.mark.parametrize("stale", [True, False], ids=["stale", "online"])
+@pytest.mark.parametrize("name", ["rigid2048_eps1e-3_k200", "g5_c5_n4096_rgb_k200", "g1_c1_n1024"])
+def test_points_fixture(cuda_ok, name, stale):
+    z, X, Y, norm = fixture_points(name)
+    rep, pot = PT.solve_points_otf(X, Y, dist(z["mu"]), dist(z["nu"]), config_of(z), normalize=norm,
+                                   stale_shift=stale)
+    assert rep.status == str(z["status"]) and rep.iterations == int(z["iterations"])
+    assert [k for k, _ in rep.error_trace] == [int(k) for k in z["trace"][:, 0]]
+    # marginal errors: same trajectory within fp32-cost noise
+    for (_, e), (_, er) in zip(rep.error_trace, z["trace"]):
+        assert abs(e - er) <= 2e-3 * abs(er) + 2e-6, (e, er)
+    scale = max(np.abs(z["alpha"]).max(), np.abs(z["beta"]).max())
+    assert np.abs(pot.alpha - z["alpha"]).max() <= RTOL * scale
+    assert np.abs(pot.beta - z["beta"]).max() <= RTOL * scale
+    assert abs(rep.transport_cost - float(z["cost"])) <= RTOL * abs(float(z["cost"]))
+
+
+def test_points_batched_equals_single(cuda_ok):
+    """A problem's result does not depend on the batch around it (bitwise)."""
+    B, n, d = 3, 700, 3
+    Xs, Ys = [], []
+    for b in range(B):
+        X, Y = O.uniform_points(n, d, 10 + b)
+        Xs.append(X)
+        Ys.append(Y)
+    cfg = lsk.SinkhornConfig(epsilon=0.01, tolerance=1e-30, max_iterations=37)
+    outs = PT.solve_points_batched(np.stack(Xs), np.stack(Ys), cfg)
+    for b in range(B):
+        rep, pot = PT.solve_points_otf(Xs[b], Ys[b], None, None, cfg)
+        rb, pb = outs[b]
+        assert rb.iterations == rep.iterations == 37 and rb.error_trace == rep.error_trace
+        np.testing.assert_array_equal(pb.alpha, pot.alpha)
+        np.testing.assert_array_equal(pb.beta, pot.beta)
+        assert rb.transport_cost == rep.transport_cost
+
+
+def test_points_batched_independent_stops(cuda_ok):
+    """Each problem stops on its own check (solver.py:286-300)."""
+    X1, Y1 = O.uniform_points(300, 2, 3)
+    X2, Y2 = O.uniform_points(300, 2, 4)
+    X2 = X2 * 0.0 + 0.5  # constant-cost problem: converges at the first check
+    Y2 = Y2 * 0.0 + 0.5
+    cfg = lsk.SinkhornConfig(epsilon=0.01, tolerance=1e-6, max_iterations=300)
+    outs = PT.solve_points_batched(np.stack([X1, X2]), np.stack([Y1, Y2]), cfg)
+    r2 = outs[1][0]
+    assert r2.status == "converged" and r2.iterations == 10
+    r1 = outs[0][0]
+    single, _ = PT.solve_points_otf(X1, Y1, None, None, cfg)
+    assert r1.iterations == single.iterations and r1.status == single.status
+
+
+def test_points_vs_oracle_ragged(cuda_ok):
+    """Shapes that are not multiples of the tiles (rows 64, chunk 2048), d=1..3."""
+    for n, m, d, eps in [(65, 2049, 1, 0.05), (130, 33, 2, 0.02), (1000, 3000, 3, 0.01)]:
+        X, _ = O.uniform_points(n, d, n)
+        _, Y = O.uniform_points(m, d, m + 1)
+        C64 = O.sq_euclidean_cost(X, Y)
+        mu_w, nu_w = np.full(n, 1.0 / n), np.full(m, 1.0 / m)
+        K = 40
+        ref = O.solve(C64, mu_w, nu_w, eps, tol=1e-30, max_iter=K, check=10)
+        rep, pot = PT.solve_points_otf(X, Y, None, None,
+                                       lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K))
+        scale = max(np.abs(ref["alpha"]).max(), np.abs(ref["beta"]).max())
+        assert np.abs(pot.alpha - ref["alpha"]).max() <= RTOL * scale, (n, m, d)
+        assert np.abs(pot.beta - ref["beta"]).max() <= RTOL * scale, (n, m, d)
+        assert abs(rep.transport_cost - ref["cost"]) <= RTOL * abs(ref["cost"])
