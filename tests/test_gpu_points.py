@@ -96,3 +96,23 @@ def test_points_vs_oracle_ragged(cuda_ok):
         assert np.abs(pot.alpha - ref["alpha"]).max() <= RTOL * scale, (n, m, d)
         assert np.abs(pot.beta - ref["beta"]).max() <= RTOL * scale, (n, m, d)
         assert abs(rep.transport_cost - ref["cost"]) <= RTOL * abs(ref["cost"])
+
+
+def test_points_sharded_one_rank_matches(cuda_ok):
+    """The sharded code path (NCCL allgathers between half-steps) with a
+    one-rank communicator is bitwise the unsharded solve."""
+    import ctypes
+
+    from paper_2605_00837_b200 import _lib
+    from paper_2605_00837_b200 import dist as D
+
+    buf = ctypes.create_string_buffer(_lib.load().lsk_nccl_unique_id_bytes())
+    _lib.call("lsk_nccl_unique_id", buf)
+    X, Y = O.uniform_points(1024, 3, 5)
+    cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=30)
+    with D.Communicator(buf.raw, 1, 0) as comm:
+        r1, p1 = PT.solve_points_otf(X, Y, None, None, cfg, normalize="max", comm=comm)
+    r0, p0 = PT.solve_points_otf(X, Y, None, None, cfg, normalize="max")
+    assert r1.error_trace == r0.error_trace and r1.transport_cost == r0.transport_cost
+    np.testing.assert_array_equal(p1.alpha, p0.alpha)
+    np.testing.assert_array_equal(p1.beta, p0.beta)
