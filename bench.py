@@ -135,12 +135,74 @@ def cpu_baseline(X, Y, iters=8):
                       f"{O.host_threads()} threads, {dt:.1f} s"}
 
 
+def other_configs():
+    """Device-timed rates of the other BASELINE configs on this GPU (parity is in
+    tests/; these are informational lines next to the C2 headline)."""
+    import torch
+
+    import paper_2605_00837_b200 as lsk
+    from paper_2605_00837_b200 import points as PT
+    from paper_2605_00837_b200 import solver as S
+
+    out = {}
+    sm, mhz = 148, 1965.0
+    mufu_pairs = 16 * sm * mhz * 1e6  # one ex2 per pair evaluation (SURVEY 8(d))
+
+    def dense(n, eps, K, seed=0):
+        rng = np.random.Generator(np.random.PCG64(seed))
+        X = rng.uniform(0.0, 1.0, (n, 2))
+        Y = rng.uniform(0.0, 1.0, (n, 2))
+        C = lsk.squared_euclidean_cost(X, Y)
+        w = lsk.make_distribution(np.ones(n))
+        lm, mu = S._dev_f32(torch, w.log_weights), S._dev_f32(torch, w.weights)
+        cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K)
+        ws = None
+        for _ in range(2):
+            r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, ws=ws)
+        torch.cuda.synchronize()
+        res = r.res.cpu().numpy()
+        return K / (r.ev0.elapsed_time(r.ev1) * 1e-3), res
+
+    v, _ = dense(1024, 1e-2, 200)
+    out["C1"] = {"workload": "dense n=m=1024 2-D points, eps=1e-2, 200 iterations", "iters_per_s": v,
+                 "ms_per_solve": 200 / v * 1e3}
+    v, res = dense(8192, 1e-4, 1000)
+    out["C3"] = {"workload": "dense n=m=8192, eps=1e-4, 1000 fixed iterations (fp32 cannot reach 1e-6, SURVEY F6)",
+                 "iters_per_s": v, "guard_stats": res[4:6].tolist()}
+    # C4: rigid pair n=m=65536 3-D, C/C.max(), eps=1e-3, on the fly, 1 GPU
+    n, K = 65536, 20
+    rng = np.random.Generator(np.random.PCG64(0))
+    X = rng.uniform(0, 1, (n, 3))
+    Y = X + rng.normal(0, 0.01, X.shape) + np.array([0.1, 0.0, 0.0])
+    cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=K)
+    for _ in range(2):
+        rep, _ = PT.solve_points_otf(X, Y, None, None, cfg, normalize="max")
+    pairs = 2.0 * n * n * K / rep.device_seconds
+    out["C4"] = {"workload": "on-the-fly 3-D points n=m=65536, C/max, eps=1e-3, 20 iterations, 1 GPU",
+                 "iters_per_s": K / rep.device_seconds, "pair_evals_per_s": pairs,
+                 "roofline": {"bound": "mufu+fp32", "frac": pairs / mufu_pairs,
+                              "peak_pair_evals_per_s": mufu_pairs, "rule": "16 ex2/clk/SM x 148 SM x 1.965 GHz"}}
+    # C5: 32 RGB problems of 4096 (one GPU's share of 256 over 8), eps=1e-2, 200 iterations
+    B, K = 32, 200
+    Xs = np.stack([np.random.Generator(np.random.PCG64(b)).uniform(0, 1, (4096, 3)) for b in range(B)])
+    Ys = np.stack([np.random.Generator(np.random.PCG64(1000 + b)).uniform(0, 1, (4096, 3)) for b in range(B)])
+    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=K)
+    for _ in range(2):
+        outs = PT.solve_points_batched(Xs, Ys, cfg)
+    dev = outs[0][0].device_seconds
+    pairs = 2.0 * B * 4096 * 4096 * K / dev
+    out["C5"] = {"workload": "32 batched on-the-fly RGB problems n=m=4096, eps=1e-2, 200 iterations (1/8 of 256)",
+                 "problem_iters_per_s": B * K / dev, "ms_per_batch": dev * 1e3, "pair_evals_per_s": pairs,
+                 "roofline": {"bound": "mufu+fp32", "frac": pairs / mufu_pairs}}
+    return out
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     X, Y = problem(0)
-    iters = max(2, int(os.environ.get("LSK_REF_ITERS", "4")))
+    iters = max(2, int(os.environ.get("LSK_REF_ITERS", "30")))
     vals = []
     cb = None
     for s in range(args.warmup + args.steps):
@@ -162,11 +224,12 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--iters", type=int, default=KITER)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other-config rate lines")
     ap.add_argument("--exact", action="store_true", help="exact two-pass variant instead of stale shift")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -249,25 +312,26 @@ def main():
            "d2h_bytes_per_step": 2 * N * 4 + 8 * 4 + 2 * 4 + (K // CHECK + 1) * 8,
            "path": "paper_2605_00837_b200.solve(CostMatrix(pinned fp64 host), ...) -> numpy potentials"}
 
-    # ---- roofline of the persistent solver kernel
+    # ---- roofline of the persistent solver kernel (SURVEY 8(d))
     peak, peak_kind = peaks()
     t_kern = float(np.mean(kern))
-    onepass = N * N * 4 * K  # compulsory bytes: C streamed once per iteration
-    twopass = 2 * N * N * 4 * K  # SURVEY 8(d) algorithmic bytes (f pass + g pass)
-    ach = onepass / t_kern / 1e9
+    twopass = 2 * N * N * 4 * K  # 8(d) algorithmic bytes: one read of C for f, one for g, per iteration
+    onepass = N * N * 4 * K      # compulsory bytes of the fused single pass (C read once per iteration)
+    ach = twopass / t_kern / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_dense_solver.json")
+    prof = os.path.join(ROOT, "profiles", "r1_dense_ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            pj = json.load(open(prof))
-            traffic = pj["dram_bytes_per_iteration"] * K
+            traffic = json.load(open(prof))["dram_bytes_per_iteration"] * K
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "traffic": traffic, "peak_kind": peak_kind,
             "kernel": "k_solve_dense (persistent cooperative solve: all K iterations, checks, cost)",
-            "bytes_per_launch": onepass, "bytes_rule": "n*m*4 per iteration (one fused pass over C)",
-            "achieved_2pass_equiv": twopass / t_kern / 1e9, "frac_2pass_equiv": twopass / t_kern / 1e9 / peak,
+            "bytes_per_launch": twopass,
+            "bytes_rule": "SURVEY 8(d): 2*n*m*4 per iteration (f pass + g pass over C); the fused kernel "
+                          "reads C once per iteration, so frac can exceed 1.0 -- see frac_compulsory",
+            "achieved_compulsory": onepass / t_kern / 1e9, "frac_compulsory": onepass / t_kern / 1e9 / peak,
             "launch_ms": t_kern * 1e3}
 
     line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
@@ -282,8 +346,10 @@ def main():
                        "guard_stats_last_step": guard},
             "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": 3 * args.steps}
+    if rank == 0 and not args.no_extra:
+        line["other_configs"] = other_configs()
     if rank == 0 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(X, Y, iters=int(os.environ.get("LSK_CPU_ITERS", "4")))
+        line["cpu_baseline"] = cpu_baseline(X, Y, iters=int(os.environ.get("LSK_CPU_ITERS", "80")))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
