@@ -50,14 +50,17 @@ extern "C" {
 const char* lsk_last_error(void);
 int32_t lsk_version(void);
 
-/* Largest m the persistent dense solver handles (8192 in this build). */
+/* Largest m the single-launch persistent dense solver handles (8192 in this
+ * build); lsk_solve_dense_f32 serves larger m with a multi-kernel loop of the
+ * half-step kernels below (same semantics, no host synchronisation). */
 int32_t lsk_solve_dense_max_cols(void);
 /* Trace capacity for a solve: ceil(max_iter / check_interval) + 1. */
 int32_t lsk_trace_capacity(int32_t max_iter, int32_t check_interval);
 size_t lsk_solve_dense_workspace_bytes(int32_t n, int32_t m);
 
 /*
- * Whole log-domain solve on a dense fp32 cost matrix, ONE cooperative launch.
+ * Whole log-domain solve on a dense fp32 cost matrix, ONE cooperative launch
+ * for m <= lsk_solve_dense_max_cols() (else an enqueued multi-kernel loop).
  * Replaces logsinkhorn.solver.solve (solver.py:230-337): alpha-first
  * alternation from zero potentials, a marginal-error check every
  * check_interval iterations (finiteness, then err, trace, stop), the extra

@@ -127,6 +127,13 @@ int32_t check_dense(const float* C, int64_t ldc, int32_t n, int32_t m) {
 
 namespace lsk_host {
 int32_t fail(int32_t code, const std::string& msg) { return ::fail(code, msg); }
+// lsk_dense_loop.cu: the multi-kernel dense solve for m beyond the persistent kernel
+size_t dense_loop_workspace_bytes(int32_t n, int32_t m);
+int32_t solve_dense_loop(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
+                         const float* log_nu, const float* mu, float inv_eps, float neg_eps, double tol,
+                         int32_t K, int32_t c, int32_t flags, float* f_out, float* g_out, int32_t* trace_iter,
+                         float* trace_err, int32_t* result, float* result_f, void* workspace,
+                         size_t workspace_bytes, cudaStream_t st);
 }  // namespace lsk_host
 
 extern "C" {
@@ -140,7 +147,8 @@ int32_t lsk_trace_capacity(int32_t max_iter, int32_t check_interval) {
 }
 
 size_t lsk_solve_dense_workspace_bytes(int32_t n, int32_t m) {
-  if (n < 1 || m < 1 || dense_width(m) == 0) return 0;
+  if (n < 1 || m < 1) return 0;
+  if (dense_width(m) == 0) return lsk_host::dense_loop_workspace_bytes(n, m);
   return dense_layout(n, m).total;
 }
 
@@ -155,7 +163,12 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
     return fail(LSK_EINVAL, "eps, tol > 0; max_iter, check_interval >= 1 required");
   if (!log_mu || !log_nu || !mu || !f_out || !g_out || !trace_iter || !trace_err || !result || !result_f)
     return fail(LSK_EINVAL, "null output/input pointer");
-  if (dense_width(m) == 0) return fail(LSK_EUNSUPPORTED, "dense solver supports m <= 8192 in this build");
+  if (dense_width(m) == 0) {  // beyond the register-resident kernel: the multi-kernel loop
+    EpsConsts e = eps_consts(eps);
+    return lsk_host::solve_dense_loop(C, ldc, n, m, log_mu, log_nu, mu, e.inv_eps, e.neg_eps, tol, max_iter,
+                                      check_interval, flags, f_out, g_out, trace_iter, trace_err, result, result_f,
+                                      workspace, workspace_bytes, S(stream));
+  }
   DenseLayout L = dense_layout(n, m);
   if (!workspace || workspace_bytes < L.total) return fail(LSK_EINVAL, "workspace too small");
   cudaStream_t st = S(stream);

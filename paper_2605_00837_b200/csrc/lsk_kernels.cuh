@@ -17,14 +17,16 @@ enum RowMode { kRowAlpha = 0, kRowCheck = 1, kRowCost = 2 };
 //   kRowCheck: out[i] = |exp(log_mu_i + LSE_j(arg4(f_i, g_j, C_ij, inv, lnu_j))) - mu_i|
 //   kRowCost : out[i] = sum_j C_ij * exp(arg4(f_i,g_j,C_ij,inv,lmu_i) + lnu_j)
 template <int MODE>
-__global__ void __launch_bounds__(256) k_row_lse(const float* __restrict__ C, long long ldc, int n, int m,
+static __global__ void __launch_bounds__(256) k_row_lse(const float* __restrict__ C, long long ldc, int n, int m,
                                                   const float* __restrict__ rowv,   // f (check/cost)
                                                   const float* __restrict__ other,  // g / beta
                                                   const float* __restrict__ lw,     // log nu
                                                   const float* __restrict__ lrow,   // log mu (check/cost)
                                                   const float* __restrict__ murow,  // mu (check)
-                                                  float inv_eps, float neg_eps, float* __restrict__ out) {
+                                                  float inv_eps, float neg_eps, float* __restrict__ out,
+                                                  const int* __restrict__ active = nullptr) {
   __shared__ float red[64];
+  if (active && !*active) return;
   const int i = blockIdx.x;
   const float* Ci = C + (long long)i * ldc;
   if (MODE == kRowCost) {
@@ -63,9 +65,11 @@ __global__ void __launch_bounds__(256) k_row_lse(const float* __restrict__ C, lo
 // CTA (bx, by) owns columns [bx*1024, +1024) (256 threads x float4, coalesced
 // 4 KB row segments) and rows [by*rs, +rs); each thread keeps a chunked online
 // (max, sumexp) per column. Partials [gridDim.y][m] are merged in fixed order.
-__global__ void __launch_bounds__(256) k_col_pairs(const float* __restrict__ C, long long ldc, int n, int m,
+static __global__ void __launch_bounds__(256) k_col_pairs(const float* __restrict__ C, long long ldc, int n, int m,
                                                     const float* __restrict__ alpha, const float* __restrict__ lmu,
-                                                    float inv_eps, int rs, float2* __restrict__ pairs) {
+                                                    float inv_eps, int rs, float2* __restrict__ pairs,
+                                                    const int* __restrict__ active = nullptr) {
+  if (active && !*active) return;
   const int j0 = (blockIdx.x * 256 + threadIdx.x) * 4;
   const int i0 = blockIdx.y * rs, i1 = min(n, i0 + rs);
   float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, sm[4] = {0.f, 0.f, 0.f, 0.f};
@@ -101,8 +105,9 @@ __global__ void __launch_bounds__(256) k_col_pairs(const float* __restrict__ C, 
     if (j0 + q < m) pairs[(size_t)blockIdx.y * m + j0 + q] = make_float2(mx[q], sm[q]);
 }
 
-__global__ void k_col_combine(const float2* __restrict__ pairs, int parts, int m, float neg_eps,
-                              float* __restrict__ out) {
+static __global__ void k_col_combine(const float2* __restrict__ pairs, int parts, int m, float neg_eps,
+                              float* __restrict__ out, const int* __restrict__ active = nullptr) {
+  if (active && !*active) return;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   float mx = -INFINITY, s = 0.f;
@@ -115,7 +120,7 @@ __global__ void k_col_combine(const float2* __restrict__ pairs, int parts, int m
 
 // Fixed-order sum of `len` floats by one CTA of 1024 threads (thread t folds
 // t, t+1024, ..., then the block tree). Writes out[0].
-__global__ void __launch_bounds__(1024) k_sum_fixed(const float* __restrict__ v, int len, float* __restrict__ out) {
+static __global__ void __launch_bounds__(1024) k_sum_fixed(const float* __restrict__ v, int len, float* __restrict__ out) {
   __shared__ float red[64];
   float s[1] = {0.f};
   for (int k = threadIdx.x; k < len; k += 1024) s[0] += v[k];
@@ -125,7 +130,7 @@ __global__ void __launch_bounds__(1024) k_sum_fixed(const float* __restrict__ v,
 
 // pi_ij = exp(fl(fl(fl(fl(fl(f_i + g_j) - C_ij) * inv) + lmu_i) + lnu_j)); counts non-finite
 // entries (materialize_plan raises NonFiniteResult, solver.py:456-457).
-__global__ void k_plan(const float* __restrict__ C, long long ldc, int n, int m, const float* __restrict__ f,
+static __global__ void k_plan(const float* __restrict__ C, long long ldc, int n, int m, const float* __restrict__ f,
                        const float* __restrict__ g, const float* __restrict__ lmu, const float* __restrict__ lnu,
                        float inv_eps, float* __restrict__ P, long long ldp, int* __restrict__ nonfinite) {
   int bad = 0;
@@ -146,7 +151,7 @@ __global__ void k_plan(const float* __restrict__ C, long long ldc, int n, int m,
 // max-normalisation (applications.py:186-188: C64 / Cmax, pass 1/Cmax as
 // scale... see below) and the single fp64->fp32 rounding of solver.py:253.
 // When `div` is non-zero the value is C64 / div (true division, as numpy).
-__global__ void k_cost_build(const double* __restrict__ X, const double* __restrict__ Y, int n, int m, int d,
+static __global__ void k_cost_build(const double* __restrict__ X, const double* __restrict__ Y, int n, int m, int d,
                              double div, float* __restrict__ C, long long ldc) {
   for (int i = blockIdx.y; i < n; i += gridDim.y)
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
@@ -162,7 +167,7 @@ __global__ void k_cost_build(const double* __restrict__ X, const double* __restr
 
 // max and min over the fp64 cost (the pipeline normalises by C.max() only if
 // max - min > 0, applications.py:186-188); per-CTA partials part[2*b], part[2*b+1]
-__global__ void k_cost_max(const double* __restrict__ X, const double* __restrict__ Y, int n, int m, int d,
+static __global__ void k_cost_max(const double* __restrict__ X, const double* __restrict__ Y, int n, int m, int d,
                            double* __restrict__ part) {
   __shared__ double red[32], redn[32];
   double mx = -1.0, mn = INFINITY;
@@ -196,13 +201,13 @@ __global__ void k_cost_max(const double* __restrict__ X, const double* __restric
 
 // dst (row stride ldd, zero-padded to ldd) = fl32(src) (row stride lds): the
 // single fp64 -> fp32 rounding of solver.py:253, done on the device.
-__global__ void k_cast_pad(const double* __restrict__ src, long long lds, int n, int m, float* __restrict__ dst,
+static __global__ void k_cast_pad(const double* __restrict__ src, long long lds, int n, int m, float* __restrict__ dst,
                            long long ldd) {
   for (int i = blockIdx.y; i < n; i += gridDim.y)
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < ldd; j += (long long)gridDim.x * blockDim.x)
       dst[(long long)i * ldd + j] = j < m ? __double2float_rn(src[(long long)i * lds + j]) : 0.f;
 }
-__global__ void k_pad_f32(const float* __restrict__ src, long long lds, int n, int m, float* __restrict__ dst,
+static __global__ void k_pad_f32(const float* __restrict__ src, long long lds, int n, int m, float* __restrict__ dst,
                           long long ldd) {
   for (int i = blockIdx.y; i < n; i += gridDim.y)
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < ldd; j += (long long)gridDim.x * blockDim.x)
@@ -210,7 +215,7 @@ __global__ void k_pad_f32(const float* __restrict__ src, long long lds, int n, i
 }
 
 // dst[i] = src[sel][i] where sel = *which (final-buffer pick after the solve)
-__global__ void k_pick(const float* __restrict__ s0, const float* __restrict__ s1, const int* __restrict__ which,
+static __global__ void k_pick(const float* __restrict__ s0, const float* __restrict__ s1, const int* __restrict__ which,
                        int len, float* __restrict__ dst) {
   const float* s = (*which) ? s1 : s0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) dst[i] = s[i];

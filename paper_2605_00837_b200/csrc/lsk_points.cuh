@@ -59,7 +59,7 @@ __device__ __forceinline__ f2 bc2(float a) { return pk2(a, a); }
 
 // One CTA = one (problem, 64-row tile of the slab, column chunk) unit.
 template <int MODE>
-__global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
+static __global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
   __shared__ __align__(16) float4 colv[kPtsChunk];
   __shared__ int tile_any;
   const int ch = blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
@@ -213,7 +213,7 @@ struct PtsCombine {
 
 // per (problem, row): combine the chunk partials in fixed order
 template <int MODE>
-__global__ void k_pts_combine(PtsCombine c) {
+static __global__ void k_pts_combine(PtsCombine c) {
   const int b = blockIdx.y;
   const int r = c.row_lo + blockIdx.x * blockDim.x + threadIdx.x;
   if (MODE == kPtsOnline && c.nflag_in && *c.nflag_in == 0) return;
@@ -265,7 +265,7 @@ __global__ void k_pts_combine(PtsCombine c) {
 }
 
 // non-finite g^k (columns) for the check's finiteness test (solver.py:287-290)
-__global__ void k_pts_colcheck(int B, int n, const float* __restrict__ pot, const int* active, int* bad) {
+static __global__ void k_pts_colcheck(int B, int n, const float* __restrict__ pot, const int* active, int* bad) {
   const int b = blockIdx.y;
   if (active && !active[b]) return;
   int any = 0;
@@ -278,7 +278,7 @@ __global__ void k_pts_colcheck(int B, int n, const float* __restrict__ pot, cons
 // The block size is independent of the number of ranks, so a sharded solve
 // sums exactly the same blocks in the same order as a single GPU.
 constexpr int kPtsBlk = 1024;
-__global__ void __launch_bounds__(1024) k_pts_blocksum(int B, int n, int lo, int hi, const float* __restrict__ v,
+static __global__ void __launch_bounds__(1024) k_pts_blocksum(int B, int n, int lo, int hi, const float* __restrict__ v,
                                                         const int* active, float* __restrict__ blk) {
   __shared__ float red[64];
   const int b = blockIdx.y, k = blockIdx.x;
@@ -307,7 +307,7 @@ struct PtsState {
 // check decision for every problem (solver.py:286-300): err = fixed-order sum
 // of the row-block sums; stop on non-finite f/g, non-finite err or err < tol.
 // kk = the iterate being checked; final = the check at the cap.
-__global__ void k_pts_decide(int B, int n, const float* __restrict__ blk, int* bad, double tol, int kk, int final,
+static __global__ void k_pts_decide(int B, int n, const float* __restrict__ blk, int* bad, double tol, int kk, int final,
                              PtsState* st, int* trace_iter, float* trace_err, int cap) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -338,7 +338,7 @@ __global__ void k_pts_decide(int B, int n, const float* __restrict__ blk, int* b
   }
 }
 
-__global__ void k_pts_cost_finish(int B, int n, const float* __restrict__ blk, PtsState* st) {
+static __global__ void k_pts_cost_finish(int B, int n, const float* __restrict__ blk, PtsState* st) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   PtsState& s = st[b];
@@ -351,7 +351,7 @@ __global__ void k_pts_cost_finish(int B, int n, const float* __restrict__ blk, P
 }
 
 // fp64 points -> float4 (x, y, z, 0) with coordinates beyond d zero
-__global__ void k_pts_pack(const double* __restrict__ P, long long count, int d, float4* __restrict__ out) {
+static __global__ void k_pts_pack(const double* __restrict__ P, long long count, int d, float4* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
     float v[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < d; ++k) v[k] = __double2float_rn(P[i * d + k]);
@@ -360,7 +360,7 @@ __global__ void k_pts_pack(const double* __restrict__ P, long long count, int d,
 }
 
 // select buffer s.fbuf into the outputs
-__global__ void k_pts_pick(int B, int n, const float* __restrict__ p0, const float* __restrict__ p1,
+static __global__ void k_pts_pick(int B, int n, const float* __restrict__ p0, const float* __restrict__ p1,
                            const PtsState* st, float* __restrict__ out) {
   const int b = blockIdx.y;
   const float* src = st[b].fbuf ? p1 : p0;

@@ -132,9 +132,6 @@ class _Solved:
 
 def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None):
     n, m = C.rows, C.cols
-    if m > _lib.load().lsk_solve_dense_max_cols():
-        raise NotImplementedError(f"dense solve with m={m} > {_lib.load().lsk_solve_dense_max_cols()} "
-                                  "columns is not in this build")
     K, c = int(config.max_iterations), int(config.check_interval)
     cap = _lib.load().lsk_trace_capacity(K, c)
     wsb = _lib.load().lsk_solve_dense_workspace_bytes(n, m)

@@ -209,3 +209,17 @@ def test_device_tensor_cost_and_outputs(cuda_ok):
     r2, p2 = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), cfg)
     assert p1.alpha.is_cuda
     np.testing.assert_array_equal(p1.alpha.cpu().numpy(), p2.alpha)
+
+
+def test_dense_wide_loop_path(cuda_ok):
+    """m > 8192: the multi-kernel dense loop, same semantics (trace, extra check
+    at a cap off the checkpoints, early stop) against the oracle."""
+    for (n, m, eps, K, tol, seed) in [(300, 9000, 0.02, 25, 1e-30, 7), (129, 8200, 0.2, 500, 1e-4, 8)]:
+        C64, mu_w, nu_w, _, _ = O.random_problem(n, m, seed)
+        r = O.solve(C64, mu_w, nu_w, eps, tol=tol, max_iter=K, check=10)
+        rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w),
+                             lsk.SinkhornConfig(epsilon=eps, tolerance=tol, max_iterations=K))
+        assert rep.status == r["status"] and rep.iterations == r["iterations"]
+        assert [k for k, _ in rep.error_trace] == [int(k) for k, _ in r["trace"]]
+        assert rel_max(pot.alpha, r["alpha"]) <= RTOL and rel_max(pot.beta, r["beta"]) <= RTOL
+        assert abs(rep.transport_cost - r["cost"]) <= RTOL * abs(r["cost"])
