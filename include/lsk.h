@@ -78,6 +78,12 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
                             int32_t* trace_iter, float* trace_err, int32_t* result, float* result_f,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* Test hook: out_k = fl(fl(fl(a_k - c_k) * inv_eps) + l_k) computed by the
+ * solver's packed argument builder (count even), to prove bitwise that no
+ * FMA contraction reaches the reference arithmetic (solver.py:77-79). */
+int32_t lsk_debug_arg3_f32(const float* a, const float* c, double eps, const float* l, float* out, int32_t count,
+                           void* stream);
+
 /* alpha = neg_eps * LSE_j((beta_j - C_ij) * inv_eps + log_nu_j)
  * -- update_alpha, solver.py:118-140 (_alpha_step 76-80). Any n, m. */
 int32_t lsk_update_alpha_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* beta,

@@ -31,6 +31,7 @@ SIGNATURES = {
     "lsk_solve_dense_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
     "lsk_solve_dense_f32": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_dbl, _c_dbl, _c_i32,
                                      _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_debug_arg3_f32": (_c_i32, [_c_p, _c_p, _c_dbl, _c_p, _c_p, _c_i32, _c_p]),
     "lsk_update_alpha_f32": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_p, _c_p]),
     "lsk_update_beta_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
     "lsk_update_beta_f32": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_p, _c_p, _c_sz, _c_p]),

@@ -61,6 +61,17 @@ __global__ void __launch_bounds__(SV::NW * 32, 1) k_solve_dense(lsk::DenseArgs a
   sv.solve();
 }
 
+// arg3x2 exactly as the solver kernels inline it, over pairs (count even)
+__global__ void k_debug_arg3(const float* a, const float* c, float inv, const float* l, float negzero, float* out,
+                             int count) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * p + 1 >= count) return;
+  const lsk::f2 inv2 = lsk::pk2(inv, inv), nz2 = lsk::pk2(negzero, negzero);
+  const lsk::f2 r = lsk::arg3x2(lsk::pk2(a[2 * p], a[2 * p + 1]), lsk::pk2(c[2 * p], c[2 * p + 1]), inv2,
+                                lsk::pk2(l[2 * p], l[2 * p + 1]), nz2);
+  lsk::up2(r, out[2 * p], out[2 * p + 1]);
+}
+
 constexpr int kHeaderInts = 64;  // [12..13]=barrier (u64) [1]=guard [2..3]=stats [4]=status [5]=iters [6]=ntrace [7]=fbuf
                                  // [8]=err(float) [9]=cost(float)
 
@@ -180,6 +191,7 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.C = C; a.ldc = ldc; a.n = n; a.m = m; a.mpad = (m + 3) / 4 * 4;
   a.log_mu = log_mu; a.log_nu = log_nu; a.mu = mu;
   a.inv_eps = ec.inv_eps; a.neg_eps = ec.neg_eps; a.tol = tol;
+  a.negzero = -0.0f;
   a.max_iter = max_iter; a.check = check_interval;
   a.stale = (flags & LSK_FLAG_STALE_SHIFT) ? 1 : 0;
   a.want_cost = (flags & LSK_FLAG_COST) ? 1 : 0;
@@ -219,6 +231,15 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   LSK_CUDA(cudaMemcpyAsync(result + 2, hdr + 6, 8, cudaMemcpyDeviceToDevice, st));
   LSK_CUDA(cudaMemcpyAsync(result + 4, hdr + 2, 8, cudaMemcpyDeviceToDevice, st));
   LSK_CUDA(cudaMemcpyAsync(result_f, hdr + 8, 8, cudaMemcpyDeviceToDevice, st));
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+int32_t lsk_debug_arg3_f32(const float* a, const float* c, double eps, const float* l, float* out, int32_t count,
+                           void* stream) {
+  if (!a || !c || !l || !out || count < 2 || (count & 1)) return fail(LSK_EINVAL, "bad debug args");
+  EpsConsts ec = eps_consts(eps);
+  k_debug_arg3<<<(count / 2 + 255) / 256, 256, 0, S(stream)>>>(a, c, ec.inv_eps, l, -0.0f, out, count);
   LSK_CUDA(cudaGetLastError());
   return LSK_OK;
 }

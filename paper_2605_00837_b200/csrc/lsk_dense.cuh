@@ -44,6 +44,7 @@ struct DenseArgs {
   const float* log_nu;
   const float* mu;
   float inv_eps, neg_eps;
+  float negzero;  // -0.0f, passed at run time (see muladd_rn2)
   double tol;
   int max_iter, check, stale, want_cost;
   // workspace (zero-initialised by the host where noted)
@@ -97,7 +98,7 @@ struct DenseSolver {
   int head_st, head_ph;            // next row to wait for
   unsigned epoch;
   int pass;                        // pass counter (sweep direction = pass & 1)
-  f2 inv2, l2e2;
+  f2 inv2, l2e2, nz2;
 
   // ---- per-thread column state (packed pairs of the columns it owns)
   f2 g2[P2];   // g_j^{k-1}
@@ -120,6 +121,7 @@ struct DenseSolver {
     pass = 0;
     inv2 = pk2(a.inv_eps, a.inv_eps);
     l2e2 = pk2(kLog2e, kLog2e);
+    nz2 = pk2(a.negzero, a.negzero);
   }
 
   __device__ __forceinline__ int col(int v, int q) const { return 4 * (v * NT + threadIdx.x) + q; }
@@ -239,7 +241,7 @@ struct DenseSolver {
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
       float x0, x1;
-      up2(arg3x2(g2[p], c[p], inv2, ln2[p]), x0, x1);
+      up2(arg3x2(g2[p], c[p], inv2, ln2[p], nz2), x0, x1);
       mx = fmax_nan(mx, fmax_nan(x0, x1));
     }
     M = block_max1(mx);
@@ -247,7 +249,7 @@ struct DenseSolver {
     const f2 nsl = pk2(-__fmul_rn(Ms, kLog2e), -__fmul_rn(Ms, kLog2e));
     f2 s2 = 0ull;
 #pragma unroll
-    for (int p = 0; p < P2; ++p) s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p]), l2e2, nsl)));
+    for (int p = 0; p < P2; ++p) s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p], nz2), l2e2, nsl)));
     float s0, s1;
     up2(s2, s0, s1);
     S = block_sum1(s0 + s1);
@@ -261,7 +263,7 @@ struct DenseSolver {
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
       float x0, x1;
-      up2(arg4x2(f2i, g2[p], c[p], inv2, ln2[p]), x0, x1);
+      up2(arg4x2(f2i, g2[p], c[p], inv2, ln2[p], nz2), x0, x1);
       mx = fmax_nan(mx, fmax_nan(x0, x1));
     }
     M = block_max1(mx);
@@ -269,7 +271,7 @@ struct DenseSolver {
     const f2 nsl = pk2(-__fmul_rn(Ms, kLog2e), -__fmul_rn(Ms, kLog2e));
     f2 s2 = 0ull;
 #pragma unroll
-    for (int p = 0; p < P2; ++p) s2 = add2(s2, ex2x2(fma2(arg4x2(f2i, g2[p], c[p], inv2, ln2[p]), l2e2, nsl)));
+    for (int p = 0; p < P2; ++p) s2 = add2(s2, ex2x2(fma2(arg4x2(f2i, g2[p], c[p], inv2, ln2[p], nz2), l2e2, nsl)));
     float s0, s1;
     up2(s2, s0, s1);
     S = block_sum1(s0 + s1);
@@ -321,8 +323,8 @@ struct DenseSolver {
     f2 s2 = 0ull, z2 = 0ull;
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
-      s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p]), l2e2, nsl)));
-      if (CHECK) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p]), l2e2)));
+      s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p], nz2), l2e2, nsl)));
+      if (CHECK) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p], nz2), l2e2)));
     }
     float s0, s1;
     up2(s2, s0, s1);
@@ -341,7 +343,7 @@ struct DenseSolver {
     const f2 fi2 = pk2(fi, fi), lm2 = pk2(lmu, lmu);
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
-      ac2[p] = add2(ac2[p], ex2x2(fma2(arg3x2(fi2, c[p], inv2, lm2), l2e2, ns2[p])));
+      ac2[p] = add2(ac2[p], ex2x2(fma2(arg3x2(fi2, c[p], inv2, lm2, nz2), l2e2, ns2[p])));
       if (SHFL && p < 5) {
         s += __shfl_xor_sync(0xffffffffu, s, 16 >> p);
         if (CHECK) z += __shfl_xor_sync(0xffffffffu, z, 16 >> p);
@@ -442,7 +444,7 @@ struct DenseSolver {
         load_row(row, c);
         f2 z2 = 0ull;
 #pragma unroll
-        for (int p = 0; p < P2; ++p) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p]), l2e2)));
+        for (int p = 0; p < P2; ++p) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p], nz2), l2e2)));
         float s0, s1;
         up2(z2, s0, s1);
         const float Sz = block_sum1(s0 + s1);
@@ -466,7 +468,7 @@ struct DenseSolver {
       load_row(row, c);
       f2 z2 = 0ull;
 #pragma unroll
-      for (int p = 0; p < P2; ++p) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p]), l2e2)));
+      for (int p = 0; p < P2; ++p) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p], nz2), l2e2)));
       float s0, s1;
       up2(z2, s0, s1);
       const float Sz = block_sum1(s0 + s1);
@@ -489,7 +491,7 @@ struct DenseSolver {
       float s = 0.f;
 #pragma unroll
       for (int p = 0; p < P2; ++p) {
-        const f2 z = add2(arg4x2(fi2, g2[p], c[p], inv2, lm2), ln2[p]);
+        const f2 z = add2(arg4x2(fi2, g2[p], c[p], inv2, lm2, nz2), ln2[p]);
         float z0, z1, c0, c1;
         up2(z, z0, z1);
         up2(c[p], c0, c1);
@@ -520,7 +522,7 @@ struct DenseSolver {
 #pragma unroll
       for (int p = 0; p < P2; ++p) {
         float y[2];
-        up2(arg3x2(fi2, c[p], inv2, lm2), y[0], y[1]);
+        up2(arg3x2(fi2, c[p], inv2, lm2, nz2), y[0], y[1]);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int e = 2 * p + h;

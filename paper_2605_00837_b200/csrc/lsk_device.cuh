@@ -292,25 +292,20 @@ __device__ __forceinline__ f2 ex2x2(f2 t) {
 __device__ __forceinline__ void lds2x2(const float* p, f2& lo, f2& hi) {
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(smem_u32(p)));
 }
-// fl(fl(u * s) + l) lane-wise with the add done as two scalar FADDs: ptxas
-// contracts a packed mul.rn.f32x2 feeding add.rn.f32x2 into one FFMA2 even
-// with -fmad=false (the .rn qualifiers do not stop it on f32x2), which would
-// break the reference's separately rounded argument build.
-// tests/test_abi.py checks the SASS for contracted argument builds.
-__device__ __forceinline__ f2 muladd_rn2(f2 u, f2 s, f2 l) {
-  float u0, u1, l0, l1;
-  up2(mul2(u, s), u0, u1);
-  up2(l, l0, l1);
-  return pk2(__fadd_rn(u0, l0), __fadd_rn(u1, l1));
-}
-__device__ __forceinline__ void lds2x2_u32(uint32_t addr, f2& lo, f2& hi) {
-  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(addr));
-}
+// fl(fl(u * s) + l) lane-wise. ptxas contracts a packed mul.rn.f32x2 feeding
+// add.rn.f32x2 into one FFMA2 even with -fmad=false (the .rn qualifiers do not
+// stop it on f32x2), which would break the reference's separately rounded
+// argument build. The product is therefore formed as
+// fma(u, s, z) with z a RUNTIME -0.0 pair (kernel argument, opaque to the
+// compiler): u*s + (-0) is exactly the rounded product (sign of zero
+// included), and an fma cannot be fused with the following add.
+// tests/test_gpu_parity.py::test_argument_build_bitwise checks the bits.
+__device__ __forceinline__ f2 muladd_rn2(f2 u, f2 s, f2 l, f2 z) { return add2(fma2(u, s, z), l); }
 // reference argument fl(fl(fl(a - c) * s) + l), lane-wise
-__device__ __forceinline__ f2 arg3x2(f2 a, f2 c, f2 s, f2 l) { return muladd_rn2(sub2(a, c), s, l); }
+__device__ __forceinline__ f2 arg3x2(f2 a, f2 c, f2 s, f2 l, f2 z) { return muladd_rn2(sub2(a, c), s, l, z); }
 // check argument fl(fl(fl(fl(f + g) - c) * s) + l), lane-wise
-__device__ __forceinline__ f2 arg4x2(f2 f, f2 g, f2 c, f2 s, f2 l) {
-  return muladd_rn2(sub2(add2(f, g), c), s, l);
+__device__ __forceinline__ f2 arg4x2(f2 f, f2 g, f2 c, f2 s, f2 l, f2 z) {
+  return muladd_rn2(sub2(add2(f, g), c), s, l, z);
 }
 }  // namespace lsk
 

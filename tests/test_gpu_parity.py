@@ -223,3 +223,25 @@ def test_dense_wide_loop_path(cuda_ok):
         assert [k for k, _ in rep.error_trace] == [int(k) for k, _ in r["trace"]]
         assert rel_max(pot.alpha, r["alpha"]) <= RTOL and rel_max(pot.beta, r["beta"]) <= RTOL
         assert abs(rep.transport_cost - r["cost"]) <= RTOL * abs(r["cost"])
+
+
+def test_argument_build_bitwise(cuda_ok):
+    """The packed argument builder reproduces numpy's separately rounded fp32
+    ops bit for bit (solver.py:77-79; an FMA here breaks eps=1e-4)."""
+    import torch
+
+    from paper_2605_00837_b200 import _lib
+
+    rng = np.random.default_rng(0)
+    k = 1 << 20
+    for eps in (1e-2, 1e-3, 1e-4):
+        a = (rng.uniform(-1, 1, k) * 1e-3).astype(np.float32)
+        c = rng.uniform(0, 2, k).astype(np.float32)
+        l = np.full(k, -np.log(8192.0), dtype=np.float32) + rng.uniform(-1, 1, k).astype(np.float32)
+        inv = np.float32(1.0) / np.float32(eps)
+        want = ((a - c) * inv) + l  # numpy fp32: three separately rounded ops
+        dev = [torch.from_numpy(x).cuda() for x in (a, c, l)]
+        out = torch.empty(k, dtype=torch.float32, device="cuda")
+        _lib.call("lsk_debug_arg3_f32", dev[0].data_ptr(), dev[1].data_ptr(), eps, dev[2].data_ptr(),
+                  out.data_ptr(), k, torch.cuda.current_stream().cuda_stream)
+        np.testing.assert_array_equal(out.cpu().numpy(), want)
