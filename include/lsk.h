@@ -166,6 +166,20 @@ int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_
                              float* f_out, float* g_out, int32_t* trace_iter, float* trace_err, int32_t* result,
                              float* result_f, void* workspace, size_t workspace_bytes, void* comm, void* stream);
 
+/* Plan consumers without the plan (f, g from a solve; pi_ij as in
+ * materialize_plan): mapped_out (B, n, d) = sum_j pi_ij y_j / sum_j pi_ij --
+ * barycentric_map, applications.py:75-97 (*zero_rows counts rows with no
+ * mass: ZeroRowMass); match_idx (B, n) = argmax_j pi_ij with the lowest j on
+ * ties and match_w = that pi_ij -- the correspondences of
+ * match_point_clouds, applications.py:195-204. Same cost/scale convention as
+ * lsk_solve_points_f32. */
+size_t lsk_points_consume_workspace_bytes(int32_t B, int32_t n, int32_t m);
+int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
+                               const float* scale, const float* f, const float* g, const float* log_mu,
+                               const float* log_nu, double eps, float* mapped_out, int32_t* match_idx,
+                               float* match_w, int32_t* zero_rows, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
 /* cmax_out[b] = max_ij sum_k (x_ik - y_jk)^2 in fp64 (device doubles), the
  * C.max() normaliser of applications.py:186-188, without materialising C. */
 int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,

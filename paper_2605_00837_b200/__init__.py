@@ -7,7 +7,9 @@ the same names, signatures and error behaviour. Kernels live in
 ``liblsk.so`` (``include/lsk.h``); there is no CPU fallback.
 """
 
+from .applications import Correspondence, barycentric_map, match_point_clouds, match_point_clouds_with_report
 from .costs import as_points, solve_points, squared_euclidean_cost
+from .points import solve_points_batched, solve_points_otf
 from .errors import (
     BackendError,
     DegenerateRange,

@@ -49,6 +49,9 @@ SIGNATURES = {
     "lsk_solve_points_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl,
                                       _c_dbl, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                       _c_sz, _c_p, _c_p]),
+    "lsk_points_consume_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
+    "lsk_points_consume_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
+                                        _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_points_cost_max": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p]),
     "lsk_nccl_unique_id_bytes": (_c_i32, []),
     "lsk_nccl_unique_id": (_c_i32, [_c_p]),

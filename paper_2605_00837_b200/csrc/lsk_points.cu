@@ -369,6 +369,49 @@ int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_
   return LSK_OK;
 }
 
+
+// ---- plan consumers without the plan
+size_t lsk_points_consume_workspace_bytes(int32_t B, int32_t n, int32_t m) {
+  if (B < 1 || n < 1 || m < 1) return 0;
+  const size_t ch = size_t(chunks_of(m));
+  return al(size_t(B) * n * 16) + al(size_t(B) * m * 16) + al(size_t(B) * ch * n * 16) + al(size_t(B) * ch * n * 8);
+}
+
+int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
+                               const float* scale, const float* f, const float* g, const float* log_mu,
+                               const float* log_nu, double eps, float* mapped_out, int32_t* match_idx,
+                               float* match_w, int32_t* zero_rows, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  if (!X || !Y || !scale || !f || !g || !log_mu || !log_nu || !mapped_out || !match_idx || !match_w || !zero_rows)
+    return pfail(LSK_EINVAL, "null pointer");
+  if (B < 1 || n < 1 || m < 1) return pfail(LSK_EINVAL, "B, n, m must be >= 1");
+  if (d < 1 || d > 3) return pfail(LSK_EUNSUPPORTED, "points consumers support d in 1..3");
+  if (!(eps > 0)) return pfail(LSK_EINVAL, "eps must be > 0");
+  if (!workspace || workspace_bytes < lsk_points_consume_workspace_bytes(B, n, m))
+    return pfail(LSK_EINVAL, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  const int chunks = chunks_of(m);
+  float4* X4 = reinterpret_cast<float4*>(ws);
+  ws += al(size_t(B) * n * 16);
+  float4* Y4 = reinterpret_cast<float4*>(ws);
+  ws += al(size_t(B) * m * 16);
+  float4* part = reinterpret_cast<float4*>(ws);
+  ws += al(size_t(B) * chunks * n * 16);
+  float2* best = reinterpret_cast<float2*>(ws);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, d, X4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, d, Y4);
+  const EpsC ec = epsc(eps);
+  lsk::PtsConsume h{B, n, m, chunks, X4, Y4, f, g, log_nu, scale, ec.inv, part, best};
+  const int tiles = (n + lsk::kPtsTileRows - 1) / lsk::kPtsTileRows;
+  lsk::k_pts_consume<<<dim3(chunks, tiles, B), lsk::kPtsThreads, 0, st>>>(h);
+  lsk::k_pts_consume_finish<<<dim3((n + 255) / 256, B), 256, 0, st>>>(B, n, m, d, chunks, part, best, X4, Y4, f, g,
+                                                                    log_mu, log_nu, scale, ec.inv, mapped_out,
+                                                                    match_idx, match_w, zero_rows);
+  P_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
 }  // extern "C"
 
 // Exact fp64 max of sum_k (x_ik - y_jk)^2 per problem (the C.max() normaliser of

@@ -369,3 +369,132 @@ static __global__ void k_pts_pick(int B, int n, const float* __restrict__ p0, co
 }
 
 }  // namespace lsk
+
+namespace lsk {
+
+// ---- plan consumers without the plan: per source row i,
+// with pi_ij = exp(((f_i + g_j) - c_ij) * inv + log mu_i + log nu_j):
+//   barycentric map  sum_j pi_ij y_j / sum_j pi_ij   (applications.py:75-97)
+//   argmax_j pi_ij, lowest j on ties                 (applications.py:195-204)
+// Row constants cancel in both, so the weights are the f-update terms
+// w_ij = 2^(A_j - K (sum d^2 - f_i / scale)) (bounded by ~1 at the solution).
+struct PtsConsume {
+  int B, n_rows, n_cols, chunks;
+  const float4* rpts;
+  const float4* cpts;
+  const float* rpot;   // f (B, n)
+  const float* cpot;   // g (B, m)
+  const float* clw;    // log nu (B, m)
+  const float* scale;
+  float inv_eps;
+  float4* part;        // (B, chunks, n): (sum w, sum w y0, sum w y1, sum w y2)
+  float2* best;        // (B, chunks, n): (max v, index as int bits)
+};
+
+static __global__ void __launch_bounds__(kPtsThreads) k_pts_consume(PtsConsume h) {
+  __shared__ __align__(16) float4 colv[kPtsChunk];
+  const int ch = blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
+  const int r_base = tile * kPtsTileRows;
+  if (r_base >= h.n_rows) return;
+  const float sc = __ldg(h.scale + b);
+  const int j0 = ch * kPtsChunk;
+  const int ncol = min(kPtsChunk, h.n_cols - j0);
+  for (int t = threadIdx.x; t < ncol; t += kPtsThreads) {
+    const size_t j = (size_t)b * h.n_cols + j0 + t;
+    float4 q = __ldg(h.cpts + j);
+    q.w = __fmul_rn(__fmaf_rn(__ldg(h.cpot + j), h.inv_eps, __ldg(h.clw + j)), kLog2e);
+    colv[t] = q;
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float x0[8], x1[8], x2[8], ini[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    int i = r_base + w * kPtsRowsPerWarp + r;
+    i = i < h.n_rows ? i : h.n_rows - 1;
+    const size_t ri = (size_t)b * h.n_rows + i;
+    const float4 x = __ldg(h.rpts + ri);
+    x0[r] = x.x; x1[r] = x.y; x2[r] = x.z;
+    ini[r] = __fdiv_rn(-__ldg(h.rpot + ri), sc);
+  }
+  const float NK = -__fmul_rn(__fmul_rn(h.inv_eps, kLog2e), sc);
+  __syncthreads();
+  float sw[8], sy0[8], sy1[8], sy2[8], bv[8];
+  int bj[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) { sw[r] = sy0[r] = sy1[r] = sy2[r] = 0.f; bv[r] = -INFINITY; bj[r] = 0x7fffffff; }
+  for (int t = lane; t < ncol; t += 32) {
+    const float4 q = colv[t];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float d0 = x0[r] - q.x, d1 = x1[r] - q.y, d2 = x2[r] - q.z;
+      const float s = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, ini[r])));
+      const float v = __fmaf_rn(s, NK, q.w);
+      const float e = ex2(v);
+      sw[r] += e;
+      sy0[r] = __fmaf_rn(e, q.x, sy0[r]);
+      sy1[r] = __fmaf_rn(e, q.y, sy1[r]);
+      sy2[r] = __fmaf_rn(e, q.z, sy2[r]);
+      if (v > bv[r]) { bv[r] = v; bj[r] = j0 + t; }  // columns visited in increasing j: first max wins
+    }
+  }
+  const size_t pbase = ((size_t)b * h.chunks + ch) * h.n_rows;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    float a0 = sw[r], a1 = sy0[r], a2 = sy1[r], a3 = sy2[r], v = bv[r];
+    int j = bj[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      a3 += __shfl_xor_sync(0xffffffffu, a3, o);
+      const float vo = __shfl_xor_sync(0xffffffffu, v, o);
+      const int jo = __shfl_xor_sync(0xffffffffu, j, o);
+      if (vo > v || (vo == v && jo < j)) { v = vo; j = jo; }
+    }
+    const int i = r_base + w * kPtsRowsPerWarp + r;
+    if (lane == 0 && i < h.n_rows) {
+      h.part[pbase + i] = make_float4(a0, a1, a2, a3);
+      h.best[pbase + i] = make_float2(v, __int_as_float(j));
+    }
+  }
+}
+
+// per row: fixed-order chunk sums -> mapped point; argmax over chunks (lowest
+// index on ties) -> target index and the plan entry pi_ij
+static __global__ void k_pts_consume_finish(int B, int n, int m, int d, int chunks, const float4* __restrict__ part,
+                                            const float2* __restrict__ best, const float4* __restrict__ rpts,
+                                            const float4* __restrict__ cpts, const float* __restrict__ f,
+                                            const float* __restrict__ g, const float* __restrict__ lmu,
+                                            const float* __restrict__ lnu, const float* __restrict__ scale,
+                                            float inv_eps, float* __restrict__ mapped, int* __restrict__ idx,
+                                            float* __restrict__ wt, int* __restrict__ zero_rows) {
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, v = -INFINITY;
+  int j = 0x7fffffff;
+  for (int ch = 0; ch < chunks; ++ch) {
+    const size_t k = ((size_t)b * chunks + ch) * n + i;
+    const float4 p = part[k];
+    a0 += p.x; a1 += p.y; a2 += p.z; a3 += p.w;
+    const float2 bb = best[k];
+    const int jj = __float_as_int(bb.y);
+    if (bb.x > v || (bb.x == v && jj < j)) { v = bb.x; j = jj; }
+  }
+  const size_t ri = (size_t)b * n + i;
+  if (!(a0 > 0.f)) atomicAdd(zero_rows, 1);  // ZeroRowMass (applications.py:92-93)
+  const float out[3] = {a1 / a0, a2 / a0, a3 / a0};
+  for (int k = 0; k < d; ++k) mapped[ri * d + k] = out[k];
+  if (j == 0x7fffffff) j = 0;
+  idx[ri] = j;
+  // pi_ij = exp(((f_i + g_j) - c_ij) * inv + lmu_i + lnu_j), c from the fp32 points
+  const float4 x = rpts[ri], y = cpts[(size_t)b * m + j];
+  const float dx = x.x - y.x, dy = x.y - y.y, dz = x.z - y.z;
+  const float c = __fmul_rn(__fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx))), __ldg(scale + b));
+  const float z = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(__fadd_rn(f[ri], g[(size_t)b * m + j]), c), inv_eps), lmu[ri]),
+                            lnu[(size_t)b * m + j]);
+  wt[ri] = expf(z);
+}
+
+}  // namespace lsk
