@@ -19,6 +19,7 @@ LSK_ECUDA = -2
 LSK_EUNSUPPORTED = -3
 LSK_FLAG_STALE_SHIFT = 1
 LSK_FLAG_COST = 2
+LSK_FLAG_TASKQ = 4
 
 _c_i32, _c_i64, _c_sz, _c_dbl, _c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_double, ctypes.c_void_p
 

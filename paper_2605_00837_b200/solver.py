@@ -130,7 +130,7 @@ class _Solved:
     __slots__ = ("f", "g", "trace_iter", "trace_err", "res", "resf", "ev0", "ev1")
 
 
-def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None):
+def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None, taskq=False):
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
     cap = _lib.load().lsk_trace_capacity(K, c)
@@ -145,6 +145,7 @@ def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=
     r.res = torch.zeros(8, dtype=torch.int32, device="cuda")
     r.resf = torch.zeros(2, dtype=torch.float32, device="cuda")
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
+    flags |= _lib.LSK_FLAG_TASKQ if taskq else 0
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
     r.ev0.record()
@@ -184,7 +185,7 @@ def _report_from(r, t0, return_device=False):
     return report, DualPotentials(alpha=alpha, beta=beta)
 
 
-def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False):
+def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, taskq=False):
     """Log-domain Sinkhorn from zero potentials (reference solver.py:230-337).
 
     Alternates f (alpha) and g (beta) updates, checks the L1 row-marginal
@@ -195,6 +196,8 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False):
     transport cost unless the solve failed. The whole loop is one
     cooperative kernel launch; the host synchronises once, at the end.
 
+    ``taskq=True`` selects the task-queue kernel (a warp per row for the f
+    update and per 128-column strip for the g update; same results contract).
     ``stale_shift=False`` selects the exact two-pass variant (max pass per
     row, exact column pass every iteration) instead of the one-pass
     stale-shift fast path; ``return_device=True`` leaves the potentials as
@@ -211,7 +214,7 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False):
     log_mu = _dev_f32(torch, mu.log_weights)
     log_nu = _dev_f32(torch, nu.log_weights)
     mu32 = _dev_f32(torch, mu.weights)
-    r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift)
+    r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift, taskq=taskq)
     return _report_from(r, t0, return_device)
 
 

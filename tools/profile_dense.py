@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--eps", type=float, default=1e-3)
     ap.add_argument("--exact", action="store_true")
+    ap.add_argument("--taskq", action="store_true")
     ap.add_argument("--reps", type=int, default=1)
     a = ap.parse_args()
     import torch
@@ -35,7 +36,7 @@ def main():
     cfg = lsk.SinkhornConfig(epsilon=a.eps, tolerance=1e-30, max_iterations=a.iters)
     ws = None
     for _ in range(a.reps):
-        r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, stale=not a.exact, ws=ws)
+        r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, stale=not a.exact, ws=ws, taskq=a.taskq)
     torch.cuda.synchronize()
     print("iters", r.res.cpu().numpy()[:6], "ms", r.ev0.elapsed_time(r.ev1), flush=True)
 
