@@ -132,8 +132,15 @@ struct DenseSolver {
   __device__ __forceinline__ void issue() {
     const uint32_t bytes = uint32_t(a.mpad) * 4u;
     const int i = row_of(iss_pass, iss_step);
+#ifndef LSK_X_NOTMA
     mbar_expect_tx(&mbar[iss_st], bytes);
     tma_load_1d(ring + size_t(iss_st) * W, a.C + (long long)i * a.ldc, bytes, &mbar[iss_st]);
+#endif
+#ifdef LSK_X_PFD
+    int P = iss_pass, q = iss_step + LSK_X_PFD;
+    while (q >= rows) { q -= rows; ++P; }
+    prefetch_l2(a.C + (long long)row_of(P, q) * a.ldc, bytes);
+#endif
   }
   __device__ __forceinline__ void advance_issue() {
     iss_st = (iss_st + 1 == STAGES) ? 0 : iss_st + 1;
@@ -156,7 +163,9 @@ struct DenseSolver {
   }
   // wait for the next row of the sequence; returns its smem copy
   __device__ __forceinline__ const float* wait_head() {
+#ifndef LSK_X_NOTMA
     mbar_wait(&mbar[head_st], uint32_t(head_ph));
+#endif
     const float* p = ring + size_t(head_st) * W;
     if (++head_st == STAGES) { head_st = 0; head_ph ^= 1; }
     return p;
@@ -323,7 +332,11 @@ struct DenseSolver {
     f2 s2 = 0ull, z2 = 0ull;
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
+#ifndef LSK_X_NOF
       s2 = add2(s2, ex2x2(fma2(arg3x2(g2[p], c[p], inv2, ln2[p], nz2), l2e2, nsl)));
+#else
+      s2 = add2(s2, c[p]);
+#endif
       if (CHECK) z2 = add2(z2, ex2x2(mul2(arg4x2(fo2, g2[p], c[p], inv2, ln2[p], nz2), l2e2)));
     }
     float s0, s1;
@@ -343,7 +356,11 @@ struct DenseSolver {
     const f2 fi2 = pk2(fi, fi), lm2 = pk2(lmu, lmu);
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
+#ifndef LSK_X_NOG
       ac2[p] = add2(ac2[p], ex2x2(fma2(arg3x2(fi2, c[p], inv2, lm2, nz2), l2e2, ns2[p])));
+#else
+      ac2[p] = add2(ac2[p], c[p]);
+#endif
       if (SHFL && p < 5) {
         s += __shfl_xor_sync(0xffffffffu, s, 16 >> p);
         if (CHECK) z += __shfl_xor_sync(0xffffffffu, z, 16 >> p);
@@ -360,7 +377,11 @@ struct DenseSolver {
   template <bool CHECK>
   __device__ __forceinline__ float f_finish(const float* row, int q, int i, float fold, float lmu, float* fnew,
                                             float& err_acc, int& bad) {
+#ifdef LSK_X_NOSUM
+    float M = __fmul_rn(-fold, a.inv_eps), S = red[kRedRows + (q & 1) * NW];
+#else
     float M = __fmul_rn(-fold, a.inv_eps), S = sum_warps(kRedRows + (q & 1) * NW);
+#endif
     if (!shift_ok(S)) {  // uniform: every thread holds the same S
       if (threadIdx.x == 0) atomicAdd(a.stats + 0, 1);
       exact_row(row, M, S);
@@ -368,30 +389,38 @@ struct DenseSolver {
     // accurate logf: lg2.approx moves f by ~1e-7 relative, which shifts the
     // marginal error near the fp32 floor enough to flip converged/not_converged
     // against the reference at err ~ tol (tests: grid64_check5)
+#ifdef LSK_X_NOLOG
+    const float fr = __fmul_rn(a.neg_eps, __fadd_rn(M, S));
+#else
     const float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
+#endif
     if (CHECK) check_row(row, i, fold, lmu, sum_warps(kRedRows + 2 * NW + (q & 1) * NW), err_acc, bad);
     if (threadIdx.x == 0) fnew[i] = fr;
     return fr;
   }
 
+  // Step q waits for row q, then finishes row q-1 (sum of the NW warp sums,
+  // accurate logf) in the same straight-line block as row q's row sums, so the
+  // finish's dependency chain overlaps the MUFU stream instead of idling it;
+  // then the column update of row q-1 with row q's butterfly interleaved; one
+  // __syncthreads; the stage of row q-1 is released.
   template <bool CHECK>
   __device__ void fused_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
     const int P = pass++;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    // scalars of the current row and (prefetched) of the next one
-    int i = row_of(P, 0);
-    float fold = ldcg(fprev + i), lmu = __ldg(a.log_mu + i);
-    int i_nx = i;
-    float fold_nx = fold, lmu_nx = lmu;
+    // scalars of rows q (cur) and q+1 (nx), prefetched one step ahead
+    int i_cur = row_of(P, 0);
+    float fold_cur = ldcg(fprev + i_cur), lmu_cur = __ldg(a.log_mu + i_cur);
+    int i_nx = i_cur;
+    float fold_nx = fold_cur, lmu_nx = lmu_cur;
     if (rows > 1) {
       i_nx = row_of(P, 1);
       fold_nx = ldcg(fprev + i_nx);
       lmu_nx = __ldg(a.log_mu + i_nx);
     }
-    // step 0: row sums of row 0 only
     const float* row = wait_head();
     float s, z = 0.f;
-    f_part<CHECK>(row, fold, s, z);
+    f_part<CHECK>(row, fold_cur, s, z);
     s = warp_sum(s);
     if (CHECK) z = warp_sum(z);
     if (lane == 0) {
@@ -399,18 +428,19 @@ struct DenseSolver {
       if (CHECK) red[kRedRows + 2 * NW + w] = z;
     }
     __syncthreads();
-    float f_prev = f_finish<CHECK>(row, 0, i, fold, lmu, fnew, err_acc, bad);
-    float lmu_prev = lmu;
     const float* row_prev = row;
+    int i_prev = i_cur;
+    float fold_prev = fold_cur, lmu_prev = lmu_cur;
     for (int q = 1; q < rows; ++q) {
-      i = i_nx; fold = fold_nx; lmu = lmu_nx;
+      i_cur = i_nx; fold_cur = fold_nx; lmu_cur = lmu_nx;
       if (q + 1 < rows) {
         i_nx = row_of(P, q + 1);
         fold_nx = ldcg(fprev + i_nx);
         lmu_nx = __ldg(a.log_mu + i_nx);
       }
       row = wait_head();
-      f_part<CHECK>(row, fold, s, z);
+      const float f_prev = f_finish<CHECK>(row_prev, q - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
+      f_part<CHECK>(row, fold_cur, s, z);
       g_part<CHECK, true>(row_prev, f_prev, lmu_prev, s, z);
       if (lane == 0) {
         red[kRedRows + (q & 1) * NW + w] = s;
@@ -418,11 +448,13 @@ struct DenseSolver {
       }
       __syncthreads();
       release();  // row q-1 fully consumed by every thread
-      f_prev = f_finish<CHECK>(row, q, i, fold, lmu, fnew, err_acc, bad);
-      lmu_prev = lmu;
       row_prev = row;
+      i_prev = i_cur;
+      fold_prev = fold_cur;
+      lmu_prev = lmu_cur;
     }
-    g_part<false, false>(row_prev, f_prev, lmu_prev, s, z);
+    const float f_last = f_finish<CHECK>(row_prev, rows - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
+    g_part<false, false>(row_prev, f_last, lmu_prev, s, z);
     __syncthreads();
     release();
   }
