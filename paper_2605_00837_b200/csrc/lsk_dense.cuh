@@ -83,13 +83,17 @@ struct DenseSolver {
   static constexpr int kRedExact = 4 * NW;
   static constexpr int kRedComb = 4 * NW + 128;
   static constexpr size_t kRedFloats = 4 * NW + 128 + 64 * NW;
-  static constexpr size_t kSmemBytes = kRingBytes + kRedFloats * sizeof(float) + STAGES * 8 + 64;
+  // mbarriers: FULL[STAGES] (TMA) + SUMS[2] (per-step warp arrivals); then STAGES release counters
+  static constexpr size_t kSmemBytes = kRingBytes + kRedFloats * sizeof(float) + (STAGES + 2) * 8 + STAGES * 4 + 64;
 
   // ---- per-CTA state
   const DenseArgs& a;
   float* ring;
   float* red;
   uint64_t* mbar;
+  uint64_t* bsum;      // SUMS[2]: NW arrivals per step (step parity picks the barrier)
+  unsigned* relc;      // [STAGES] warps done with the row in each stage
+  unsigned gstep;      // fused steps so far (barrier / phase selection)
   int b, G, r0, r1, rows;
   // TMA ring, tracked incrementally (no 64-bit div/mod on the hot path):
   // the producer (thread 0) walks the global row sequence pass by pass; the
@@ -110,6 +114,9 @@ struct DenseSolver {
     ring = reinterpret_cast<float*>(smem);
     red = reinterpret_cast<float*>(smem + kRingBytes);
     mbar = reinterpret_cast<uint64_t*>(smem + kRingBytes + kRedFloats * sizeof(float));
+    bsum = mbar + STAGES;
+    relc = reinterpret_cast<unsigned*>(bsum + 2);
+    gstep = 0;
     b = blockIdx.x;
     G = gridDim.x;
     r0 = int((long long)b * a.n / G);
@@ -152,6 +159,9 @@ struct DenseSolver {
     for (size_t k = threadIdx.x; k < kRingBytes / 16; k += NT) r4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (threadIdx.x == 0) {
       for (int s = 0; s < STAGES; ++s) mbar_init(&mbar[s], 1);
+      mbar_init(&bsum[0], NW);
+      mbar_init(&bsum[1], NW);
+      for (int s = 0; s < STAGES; ++s) relc[s] = 0;
       fence_mbar_init();
     }
     __syncthreads();
@@ -404,10 +414,54 @@ struct DenseSolver {
   // finish's dependency chain overlaps the MUFU stream instead of idling it;
   // then the column update of row q-1 with row q's butterfly interleaved; one
   // __syncthreads; the stage of row q-1 is released.
+  // No block barrier per row: each warp posts its row sums with an mbarrier
+  // arrival (SUMS[step & 1]); a warp waits for step q-1's arrivals only when it
+  // needs row q-1's total (at step q). The stage of row q-1 is refilled by the
+  // last warp to finish with it (shared-memory counter). Warps drift by at most
+  // one step, so the double-buffered sums and two barriers suffice.
+  __device__ __forceinline__ void post(unsigned step, float s, float z, bool check) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+      red[kRedRows + (step & 1) * NW + w] = s;
+      if (check) red[kRedRows + 2 * NW + (step & 1) * NW + w] = z;
+      mbar_arrive(&bsum[step & 1]);
+    }
+  }
+  __device__ __forceinline__ void wait_posted(unsigned step) {
+    mbar_wait(&bsum[step & 1], (step >> 1) & 1);
+  }
+  // this warp is done with row (P, q) held in stage st; the last warp to be
+  // done refills the stage with the row STAGES positions later in the sequence
+  __device__ __forceinline__ void release_warp(int st, int P, int q) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0 && atom_add_acqrel_smem(&relc[st], 1u) == unsigned(NW - 1)) {
+      relc[st] = 0;
+      q += STAGES;
+      while (q >= rows) { q -= rows; ++P; }
+      const uint32_t bytes = uint32_t(a.mpad) * 4u;
+      fence_proxy_async();
+      mbar_expect_tx(&mbar[st], bytes);
+      tma_load_1d(ring + size_t(st) * W, a.C + (long long)row_of(P, q) * a.ldc, bytes, &mbar[st]);
+    }
+  }
+
+  template <bool CHECK>
+  __device__ __forceinline__ float f_finish_async(const float* row, unsigned step, int i, float fold, float lmu,
+                                                  float* fnew, float& err_acc, int& bad) {
+    float M = __fmul_rn(-fold, a.inv_eps), S = sum_warps(kRedRows + (step & 1) * NW);
+    if (!shift_ok(S)) {  // uniform: every thread holds the same S
+      if (threadIdx.x == 0) atomicAdd(a.stats + 0, 1);
+      exact_row(row, M, S);
+    }
+    const float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
+    if (CHECK) check_row(row, i, fold, lmu, sum_warps(kRedRows + 2 * NW + (step & 1) * NW), err_acc, bad);
+    if (threadIdx.x == 0) fnew[i] = fr;
+    return fr;
+  }
+
   template <bool CHECK>
   __device__ void fused_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
     const int P = pass++;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     // scalars of rows q (cur) and q+1 (nx), prefetched one step ahead
     int i_cur = row_of(P, 0);
     float fold_cur = ldcg(fprev + i_cur), lmu_cur = __ldg(a.log_mu + i_cur);
@@ -418,17 +472,16 @@ struct DenseSolver {
       fold_nx = ldcg(fprev + i_nx);
       lmu_nx = __ldg(a.log_mu + i_nx);
     }
+    const unsigned g0 = gstep;
+    int st_cur = head_st;
     const float* row = wait_head();
     float s, z = 0.f;
     f_part<CHECK>(row, fold_cur, s, z);
     s = warp_sum(s);
     if (CHECK) z = warp_sum(z);
-    if (lane == 0) {
-      red[kRedRows + w] = s;
-      if (CHECK) red[kRedRows + 2 * NW + w] = z;
-    }
-    __syncthreads();
+    post(g0, s, z, CHECK);
     const float* row_prev = row;
+    int st_prev = st_cur;
     int i_prev = i_cur;
     float fold_prev = fold_cur, lmu_prev = lmu_cur;
     for (int q = 1; q < rows; ++q) {
@@ -438,27 +491,35 @@ struct DenseSolver {
         fold_nx = ldcg(fprev + i_nx);
         lmu_nx = __ldg(a.log_mu + i_nx);
       }
+      st_cur = head_st;
       row = wait_head();
-      const float f_prev = f_finish<CHECK>(row_prev, q - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
+      wait_posted(g0 + q - 1);
+      const float f_prev = f_finish_async<CHECK>(row_prev, g0 + q - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
       f_part<CHECK>(row, fold_cur, s, z);
       g_part<CHECK, true>(row_prev, f_prev, lmu_prev, s, z);
-      if (lane == 0) {
-        red[kRedRows + (q & 1) * NW + w] = s;
-        if (CHECK) red[kRedRows + 2 * NW + (q & 1) * NW + w] = z;
-      }
-      __syncthreads();
-      release();  // row q-1 fully consumed by every thread
+      post(g0 + q, s, z, CHECK);
+      release_warp(st_prev, P, q - 1);  // this warp is done with row q-1
       row_prev = row;
+      st_prev = st_cur;
       i_prev = i_cur;
       fold_prev = fold_cur;
       lmu_prev = lmu_cur;
     }
-    const float f_last = f_finish<CHECK>(row_prev, rows - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
+    wait_posted(g0 + rows - 1);
+    const float f_last = f_finish_async<CHECK>(row_prev, g0 + rows - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
     g_part<false, false>(row_prev, f_last, lmu_prev, s, z);
+    release_warp(st_prev, P, rows - 1);
+    gstep = g0 + rows;
+    // the barrier-synchronised passes resume the ring cursor after this pass
+    {
+      int q2 = rows + STAGES, P2_ = P;
+      while (q2 >= rows) { q2 -= rows; ++P2_; }
+      iss_pass = P2_;
+      iss_step = q2;
+      iss_st = head_st;
+    }
     __syncthreads();
-    release();
   }
-
   // ================= exact row pass (two-pass max/sum from the on-chip row) ========
   template <bool CHECK>
   __device__ void row_exact_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
