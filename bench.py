@@ -148,27 +148,45 @@ def other_configs():
     sm, mhz = 148, 1965.0
     mufu_pairs = 16 * sm * mhz * 1e6  # one ex2 per pair evaluation
 
-    def dense(n, eps, K, seed=0):
+    def dense(n, eps, K, seed=0, tol=1e-30, reps=2):
         rng = np.random.Generator(np.random.PCG64(seed))
         X = rng.uniform(0.0, 1.0, (n, 2))
         Y = rng.uniform(0.0, 1.0, (n, 2))
         C = lsk.squared_euclidean_cost(X, Y)
         w = lsk.make_distribution(np.ones(n))
         lm, mu = S._dev_f32(torch, w.log_weights), S._dev_f32(torch, w.weights)
-        cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K)
+        cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=tol, max_iterations=K)
         ws = None
-        for _ in range(2):
+        for _ in range(reps):
             r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, ws=ws)
         torch.cuda.synchronize()
         res = r.res.cpu().numpy()
-        return K / (r.ev0.elapsed_time(r.ev1) * 1e-3), res
+        sec = r.ev0.elapsed_time(r.ev1) * 1e-3
+        if tol > 1e-29:
+            nt = int(res[2])
+            te = r.trace_err[:nt].cpu().numpy()
+            return {"tolerance": tol, "status": ["not_converged", "converged", "numerical_failure"][int(res[0])],
+                    "iterations": int(res[1]), "final_err": float(r.resf[0].item()),
+                    "min_err_seen": float(te.min()) if nt else None, "time_ms": sec * 1e3}
+        return int(res[1]) / sec, res
+
+    def time_to_tol(n, eps, K, tols):
+        out = []
+        for t in tols:
+            d = dense(n, eps, K, tol=t, reps=1)
+            out.append(d)
+            if d["status"] == "converged":
+                break
+        return out
 
     v, _ = dense(1024, 1e-2, 200)
     out["C1"] = {"workload": "dense n=m=1024 2-D points, eps=1e-2, 200 iterations", "iters_per_s": v,
                  "ms_per_solve": 200 / v * 1e3}
     v, res = dense(8192, 1e-4, 1000)
     out["C3"] = {"workload": "dense n=m=8192, eps=1e-4, 1000 fixed iterations (fp32 cannot reach 1e-6, SURVEY F6)",
-                 "iters_per_s": v, "guard_stats": res[4:6].tolist()}
+                 "iters_per_s": v, "guard_stats": res[4:6].tolist(),
+                 "time_to_tolerance": time_to_tol(8192, 1e-4, 30000, [1e-6])}
+    out["C2_time_to_tolerance"] = time_to_tol(8192, 1e-3, 20000, [1e-6, 1e-5])
     # C4: rigid pair n=m=65536 3-D, C/C.max(), eps=1e-3, on the fly, 1 GPU
     n, K = 65536, 20
     rng = np.random.Generator(np.random.PCG64(0))

@@ -140,6 +140,35 @@ int32_t lsk_cast_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int3
 
 
 /* ---------------------------------------------------------------------------
+ * fp64 (precision="double"; half-steps with float64 potentials, solver.py:60-65):
+ * the same entry points in double with the reference's double arithmetic
+ * (inv_eps = 1.0/eps, separately rounded ops, full-precision exp/log). C is a
+ * row-major fp64 matrix (row stride ldc >= m, no alignment needs); all other
+ * arrays double except trace_iter/result (int32). The solve is the exact
+ * two-pass multi-kernel loop; result_f holds (final error, cost) as doubles. */
+size_t lsk_solve_dense_f64_workspace_bytes(int32_t n, int32_t m);
+int32_t lsk_solve_dense_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* log_mu,
+                            const double* log_nu, const double* mu, double eps, double tol, int32_t max_iter,
+                            int32_t check_interval, int32_t flags, double* f_out, double* g_out, int32_t* trace_iter,
+                            double* trace_err, int32_t* result, double* result_f, void* workspace,
+                            size_t workspace_bytes, void* stream);
+int32_t lsk_update_alpha_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* beta,
+                             const double* log_nu, double eps, double* alpha_out, void* stream);
+size_t lsk_update_beta_f64_workspace_bytes(int32_t n, int32_t m);
+int32_t lsk_update_beta_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* alpha,
+                            const double* log_mu, double eps, double* beta_out, void* workspace,
+                            size_t workspace_bytes, void* stream);
+int32_t lsk_marginal_error_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* mu,
+                               const double* log_mu, const double* log_nu, const double* alpha, const double* beta,
+                               double eps, double* err_out, void* workspace, size_t workspace_bytes, void* stream);
+int32_t lsk_transport_cost_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* log_mu,
+                               const double* log_nu, const double* alpha, const double* beta, double eps,
+                               double* cost_out, void* workspace, size_t workspace_bytes, void* stream);
+int32_t lsk_materialize_plan_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* log_mu,
+                                 const double* log_nu, const double* alpha, const double* beta, double eps, double* P,
+                                 int64_t ldp, int32_t* nonfinite_out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * On-the-fly point-cloud solver (configs C4/C5): the squared-Euclidean cost is
  * recomputed in registers from fp32 points and never stored.
  *

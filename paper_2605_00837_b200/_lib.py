@@ -46,6 +46,18 @@ SIGNATURES = {
     "lsk_build_cost_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p,
                                     _c_sz, _c_p]),
     "lsk_cast_cost_f32": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_p]),
+    "lsk_solve_dense_f64_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
+    "lsk_solve_dense_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_dbl, _c_dbl, _c_i32, _c_i32,
+                                     _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_update_alpha_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_p, _c_p]),
+    "lsk_update_beta_f64_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
+    "lsk_update_beta_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_marginal_error_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_dbl, _c_p,
+                                        _c_p, _c_sz, _c_p]),
+    "lsk_transport_cost_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl, _c_p, _c_p,
+                                        _c_sz, _c_p]),
+    "lsk_materialize_plan_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl, _c_p,
+                                          _c_i64, _c_p, _c_p]),
     "lsk_solve_points_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_solve_points_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl,
                                       _c_dbl, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,

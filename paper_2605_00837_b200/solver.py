@@ -19,6 +19,7 @@ import time
 import numpy as np
 
 from . import _lib
+from . import solver64 as _s64
 from .errors import BackendError, DimensionMismatch, NonFiniteResult
 from .types import (
     _STATUS_BY_CODE,
@@ -69,15 +70,10 @@ def _dev_f32(torch, x):
     return torch.from_numpy(np.ascontiguousarray(np.asarray(x), dtype=np.float32)).to("cuda")
 
 
-def _check_precision(*arrays):
-    for a in arrays:
-        dt = getattr(a, "dtype", None)
-        if dt is None:
-            continue
-        name = str(dt)
-        if "float64" in name or name == "double":
-            raise NotImplementedError(
-                "float64 potentials: the B200 path computes in fp32 (precision='single')")
+def _is_f64(*arrays):
+    """The reference's dtype rule (solver.py:60-65): the first float32/float64
+    argument decides, anything else means float64."""
+    return _s64.float_dtype(*arrays) == np.float64
 
 
 def to_device_cost(cost):
@@ -206,8 +202,9 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, taskq=
     both half-steps; results are bit-identical either way).
     """
     _check_dims(cost, mu, nu)
-    if config.precision != "single":
-        raise NotImplementedError("precision='double' is not available on the B200 path (fp32 only)")
+    if config.precision == "double":  # the reference's float64 path (types.py:168-170)
+        _torch()
+        return _s64.solve(cost, mu, nu, config, return_device)
     torch = _torch()
     t0 = time.perf_counter()
     C = to_device_cost(cost)
@@ -225,9 +222,10 @@ def _half_inputs(cost, eps):
 
 
 def update_alpha(cost, nu, beta, eps, plan=ReductionPlan()):
-    """One alpha half-step (reference solver.py:118-140), fp32."""
-    _check_precision(beta)
+    """One alpha half-step (reference solver.py:118-140) in the dtype of beta."""
     torch = _half_inputs(cost, eps)
+    if _is_f64(beta):
+        return _s64.update_alpha(cost, nu, beta, eps)
     C = to_device_cost(cost)
     b, lnu = _vecs(torch, beta, nu.log_weights)
     out = torch.empty(C.rows, dtype=torch.float32, device="cuda")
@@ -243,8 +241,14 @@ def update_beta(cost, mu, alpha, eps, plan=ReductionPlan(), transposed_cost=None
     same coalesced column kernel over C, so the strided and transposed
     results are bit-identical, as the reference guarantees.
     """
-    _check_precision(alpha)
     torch = _half_inputs(cost, eps)
+    if transposed_cost is not None:
+        shp = tuple(np.shape(transposed_cost)) if not hasattr(transposed_cost, "shape") else tuple(transposed_cost.shape)
+        rows, cols = (cost.rows, cost.cols)
+        if shp != (cols, rows):
+            raise DimensionMismatch(f"transposed_cost has shape {shp}, expected {(cols, rows)}")
+    if _is_f64(alpha):
+        return _s64.update_beta(cost, mu, alpha, eps)
     C = to_device_cost(cost)
     if transposed_cost is not None:
         shp = tuple(np.shape(transposed_cost)) if not hasattr(transposed_cost, "shape") else tuple(transposed_cost.shape)
@@ -267,8 +271,9 @@ def _vecs(torch, *xs):
 
 def marginal_error(cost, mu, nu, alpha, beta, eps, plan=ReductionPlan()):
     """L1 row-marginal error of (alpha, beta) (reference solver.py:179-206)."""
-    _check_precision(alpha, beta)
     torch = _half_inputs(cost, eps)
+    if _is_f64(alpha, beta):
+        return _s64.marginal_error(cost, mu, nu, alpha, beta, eps)
     C = to_device_cost(cost)
     w, lmu, lnu, a, b = _vecs(torch, mu.weights, mu.log_weights, nu.log_weights, alpha, beta)
     ws = torch.empty(C.rows, dtype=torch.float32, device="cuda")
@@ -280,8 +285,9 @@ def marginal_error(cost, mu, nu, alpha, beta, eps, plan=ReductionPlan()):
 
 def transport_cost(cost, mu, nu, alpha, beta, eps, plan=ReductionPlan()):
     """Plan-weighted total cost (reference solver.py:209-227)."""
-    _check_precision(alpha, beta)
     torch = _half_inputs(cost, eps)
+    if _is_f64(alpha, beta):
+        return _s64.transport_cost(cost, mu, nu, alpha, beta, eps)
     C = to_device_cost(cost)
     lmu, lnu, a, b = _vecs(torch, mu.log_weights, nu.log_weights, alpha, beta)
     ws = torch.empty(C.rows, dtype=torch.float32, device="cuda")
@@ -296,8 +302,9 @@ def materialize_plan(cost, mu, nu, alpha, beta, eps, *, return_device=False):
 
     Raises NonFiniteResult if any entry is NaN or infinite.
     """
-    _check_precision(alpha, beta)
     torch = _half_inputs(cost, eps)
+    if _is_f64(alpha, beta):
+        return _s64.materialize_plan(cost, mu, nu, alpha, beta, eps, return_device)
     C = to_device_cost(cost)
     lmu, lnu, a, b = _vecs(torch, mu.log_weights, nu.log_weights, alpha, beta)
     P = torch.empty((C.rows, C.cols), dtype=torch.float32, device="cuda")

@@ -40,9 +40,9 @@ def save(name, **kw):
     print(f"wrote {path} ({os.path.getsize(path)} B)")
 
 
-def solve_case(name, cost, mu, nu, eps, K, tol=1e-30, check=10, extra=None):
+def solve_case(name, cost, mu, nu, eps, K, tol=1e-30, check=10, extra=None, precision="single"):
     cfg = ls.SinkhornConfig(epsilon=eps, tolerance=tol, max_iterations=K,
-                            check_interval=check, precision="single")
+                            check_interval=check, precision=precision)
     t = time.perf_counter()
     rep, pot = ls.solve(cost, mu, nu, cfg)
     dt = time.perf_counter() - t
@@ -117,6 +117,40 @@ def small_cases():
                extra=dict(C=cost.values))
 
 
+def double_cases():
+    """precision="double" solves and float64 half-steps (reference dt = float64)."""
+    mu, nu, cost = ls.generate_grid_problem(64, 64, 0)
+    solve_case("dbl_grid64_eps1e-3", cost, mu, nu, 0.001, K=10000, tol=1e-6, extra=dict(grid=(64, 64, 0)),
+               precision="double")
+    mu, nu, cost = ls.generate_grid_problem(40, 70, 1)
+    solve_case("dbl_grid40x70_cap25", cost, mu, nu, 0.05, K=25, tol=1e-12, extra=dict(grid=(40, 70, 1)),
+               precision="double")
+    C, mu_w, nu_w, _, _ = lsk_oracle.random_problem(257, 300, 3)
+    solve_case("dbl_rand_257x300", ls.make_cost_matrix(257, 300, C.ravel()), ls.make_distribution(mu_w),
+               ls.make_distribution(nu_w), 0.05, K=57, extra=dict(seed=3, shape=(257, 300)), precision="double")
+    cost = ls.make_cost_matrix(2, 2, [0.0, 1.0, 1.0, 0.0])
+    half = ls.make_distribution([0.5, 0.5])
+    solve_case("dbl_antidiag", cost, half, half, 0.1, K=10000, tol=1e-9, extra=dict(C=cost.values),
+               precision="double")
+    out = {}
+    for (n, m) in [(8, 8), (37, 53), (300, 1000)]:
+        C, mu_w, nu_w, alpha_in, beta = lsk_oracle.random_problem(n, m, 200 + n + m)
+        alpha_in, beta = alpha_in.astype(np.float64), beta.astype(np.float64)
+        cost = ls.make_cost_matrix(n, m, C.ravel())
+        mu, nu = ls.make_distribution(mu_w), ls.make_distribution(nu_w)
+        key = f"{n}x{m}"
+        out[key + "_alpha"] = ls.update_alpha(cost, nu, beta, 0.05)
+        out[key + "_beta_out"] = ls.update_beta(cost, mu, alpha_in, 0.05)
+        out[key + "_merr"] = ls.marginal_error(cost, mu, nu, alpha_in, beta, 0.05)
+        out[key + "_tcost"] = ls.transport_cost(cost, mu, nu, alpha_in, beta, 0.05)
+        P = ls.materialize_plan(cost, mu, nu, alpha_in, beta, 0.05).values
+        out[key + "_plan_rows"] = P.sum(axis=1)
+        out[key + "_plan_corner"] = P[:4, :4]
+    out["shapes"] = np.array([(8, 8), (37, 53), (300, 1000)])
+    out["eps"] = 0.05
+    save("dbl_half_steps", **out)
+
+
 def half_step_cases():
     out = {}
     shapes = [(1, 1), (8, 8), (37, 53), (300, 1000), (1031, 517)]
@@ -173,5 +207,6 @@ if __name__ == "__main__":
     else:
         small_cases()
         half_step_cases()
+        double_cases()
         if a.big:
             big_cases()

@@ -113,3 +113,14 @@ def test_oracle_vs_live_reference_random():
         np.testing.assert_array_equal(r["alpha"], pot.alpha)
         np.testing.assert_array_equal(r["beta"], pot.beta)
         assert r["trace"] == rep.error_trace and r["cost"] == rep.transport_cost
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("dbl_") if n != "dbl_half_steps"])
+def test_oracle_double_matches_reference(name):
+    """The oracle's float64 path reproduces the reference's precision="double" solve."""
+    z, C64, mu_w, nu_w = fixture_problem(name)
+    r = O.solve(C64, mu_w, nu_w, float(z["eps"]), tol=float(z["tol"]), max_iter=int(z["K"]),
+                check=int(z["check"]), dtype=np.float64)
+    assert r["status"] == str(z["status"]) and r["iterations"] == int(z["iterations"])
+    np.testing.assert_allclose(r["alpha"], z["alpha"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(r["beta"], z["beta"], rtol=0, atol=1e-14)
