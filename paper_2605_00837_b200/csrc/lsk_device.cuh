@@ -189,6 +189,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
   }
 }
+// spin variant for short hand-offs between warps of one CTA: plain try_wait
+// (hardware-suspending, no nanosleep), watchdog checked only every 4096 tries
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t tries = 0;
+  uint64_t t0 = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    if ((++tries & 4095u) == 0) {
+      const uint64_t now = globaltimer_ns();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > kSpinTimeoutNs) __trap();
+    }
+  }
+}
 __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes,
                                             uint64_t* bar) {
   asm volatile(
