@@ -94,6 +94,10 @@ struct DenseSolver {
   uint64_t* bsum;      // SUMS[2]: NW arrivals per step (step parity picks the barrier)
   unsigned* relc;      // [STAGES] warps done with the row in each stage
   unsigned gstep;      // fused steps so far (barrier / phase selection)
+  // f and log mu of the last two rows of the previous fused pass: the first two
+  // rows of the next pass when it is the very next pass (sweeps alternate)
+  float carry_f0, carry_f1, carry_l0, carry_l1;
+  int carry_pass;
   int b, G, r0, r1, rows;
   // TMA ring, tracked incrementally (no 64-bit div/mod on the hot path):
   // the producer (thread 0) walks the global row sequence pass by pass; the
@@ -117,6 +121,7 @@ struct DenseSolver {
     bsum = mbar + STAGES;
     relc = reinterpret_cast<unsigned*>(bsum + 2);
     gstep = 0;
+    carry_pass = -1;
     b = blockIdx.x;
     G = gridDim.x;
     r0 = int((long long)b * a.n / G);
@@ -460,15 +465,19 @@ struct DenseSolver {
   template <bool CHECK>
   __device__ void fused_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
     const int P = pass++;
-    // scalars of rows q (cur) and q+1 (nx), prefetched one step ahead
+    // scalars of rows q (cur) and q+1 (nx), prefetched one step ahead; the
+    // first two come from the previous pass's registers when it was pass P-1
     int i_cur = row_of(P, 0);
-    float fold_cur = ldcg(fprev + i_cur), lmu_cur = __ldg(a.log_mu + i_cur);
-    int i_nx = i_cur;
-    float fold_nx = fold_cur, lmu_nx = lmu_cur;
-    if (rows > 1) {
-      i_nx = row_of(P, 1);
-      fold_nx = ldcg(fprev + i_nx);
-      lmu_nx = __ldg(a.log_mu + i_nx);
+    int i_nx = rows > 1 ? row_of(P, 1) : i_cur;
+    float fold_cur, lmu_cur, fold_nx, lmu_nx;
+    if (carry_pass == P && rows > 1) {
+      fold_cur = carry_f0; lmu_cur = carry_l0;
+      fold_nx = carry_f1; lmu_nx = carry_l1;
+    } else {
+      fold_cur = ldcg(fprev + i_cur);
+      lmu_cur = __ldg(a.log_mu + i_cur);
+      fold_nx = rows > 1 ? ldcg(fprev + i_nx) : fold_cur;
+      lmu_nx = rows > 1 ? __ldg(a.log_mu + i_nx) : lmu_cur;
     }
     const unsigned g0 = gstep;
     int st_cur = head_st;
@@ -497,6 +506,8 @@ struct DenseSolver {
       const float f_prev = f_finish_async<CHECK>(row_prev, g0 + q - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
       f_part<CHECK>(row, fold_cur, s, z);
       g_part<CHECK, true>(row_prev, f_prev, lmu_prev, s, z);
+      carry_f1 = f_prev;
+      carry_l1 = lmu_prev;
       post(g0 + q, s, z, CHECK);
       release_warp(st_prev, P, q - 1);  // this warp is done with row q-1
       row_prev = row;
@@ -510,6 +521,9 @@ struct DenseSolver {
     g_part<false, false>(row_prev, f_last, lmu_prev, s, z);
     release_warp(st_prev, P, rows - 1);
     gstep = g0 + rows;
+    carry_f0 = f_last;
+    carry_l0 = lmu_prev;
+    carry_pass = rows > 1 ? P + 1 : -1;
     // the barrier-synchronised passes resume the ring cursor after this pass
     {
       int q2 = rows + STAGES, P2_ = P;
@@ -524,6 +538,7 @@ struct DenseSolver {
   template <bool CHECK>
   __device__ void row_exact_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
     const int P = pass++;
+    carry_pass = -1;  // f changes outside the fused pass
     for (int q = 0; q < rows; ++q) {
       const int i = row_of(P, q);
       const float* row = wait_head();
@@ -658,39 +673,40 @@ struct DenseSolver {
   // ---- column combines: CTA b handles 32-column groups b, b+G, ...; the NW
   // warps split the G partial rows into contiguous ranges, then a fixed
   // halving tree over the NW range sums (in smem) finishes each column.
+  // Column combine, balanced over the grid: CTA b owns the contiguous columns
+  // [b m/G, (b+1) m/G); its threads are (column, slice) pairs -- slice q of
+  // QS sums the partial rows k = q, q + QS, ... of its column with all loads
+  // in flight at once -- then one thread per column adds the QS slice sums in
+  // order (deterministic) and finishes g_j.
   __device__ void combine_stale(const float* gold, float* gnew, int k) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int ngroups = (a.m + 31) / 32;
-    float* cr = red + kRedComb;
+    const int j0 = int((long long)b * a.m / G), j1 = int((long long)(b + 1) * a.m / G);
+    const int nc = j1 - j0;
+    float* cr = red + kRedComb;  // [QS][nc] slice sums (64*NW floats available)
+    const int QS = nc > 0 ? min(NT / nc, (64 * NW) / nc) : 1;
+    const int t = threadIdx.x;
     bool fired = false;
-    for (int grp = b; grp < ngroups; grp += G) {
-      const int j = grp * 32 + lane;
-      const int k0 = w * G / NW, k1 = (w + 1) * G / NW;
+    if (nc > 0 && QS >= 1 && t < QS * nc) {
+      const int c = t % nc, q = t / nc, j = j0 + c;
       float s = 0.f;
-      if (j < a.m) {
-        int kk = k0;
-        for (; kk + 4 <= k1; kk += 4) {
-          const float v0 = ldcg(a.part + (size_t)kk * W + j), v1 = ldcg(a.part + (size_t)(kk + 1) * W + j);
-          const float v2 = ldcg(a.part + (size_t)(kk + 2) * W + j), v3 = ldcg(a.part + (size_t)(kk + 3) * W + j);
-          s += (v0 + v1) + (v2 + v3);
-        }
-        for (; kk < k1; ++kk) s += ldcg(a.part + (size_t)kk * W + j);
+      int kk = q;
+      for (; kk + 3 * QS < G; kk += 4 * QS) {
+        const float v0 = ldcg(a.part + (size_t)kk * W + j), v1 = ldcg(a.part + (size_t)(kk + QS) * W + j);
+        const float v2 = ldcg(a.part + (size_t)(kk + 2 * QS) * W + j), v3 = ldcg(a.part + (size_t)(kk + 3 * QS) * W + j);
+        s += (v0 + v1) + (v2 + v3);
       }
-      cr[w * 32 + lane] = s;
-      __syncthreads();
-      if (w == 0) {
-        for (int h = NW / 2; h >= 1; h >>= 1)
-          for (int u = 0; u < h; ++u) cr[u * 32 + lane] += cr[(u + h) * 32 + lane];
-        if (j < a.m) {
-          const float sj = __fmul_rn(-ldcg(gold + j), a.inv_eps);
-          const float S = cr[lane];
-          if (!shift_ok(S)) fired = true;
-          gnew[j] = __fmul_rn(a.neg_eps, lse_finish(sj, S));
-        }
-      }
-      __syncthreads();
+      for (; kk < G; kk += QS) s += ldcg(a.part + (size_t)kk * W + j);
+      cr[q * nc + c] = s;
     }
-    if (w == 0 && __any_sync(0xffffffffu, fired) && lane == 0) atomicMax(a.guard, k);
+    const float gj = (t < nc) ? ldcg(gold + j0 + t) : 0.f;  // issued before the barrier
+    __syncthreads();
+    if (t < nc) {
+      float S = 0.f;
+      for (int q = 0; q < QS; ++q) S += cr[q * nc + t];
+      const float sj = __fmul_rn(-gj, a.inv_eps);
+      if (!shift_ok(S)) fired = true;
+      gnew[j0 + t] = __fmul_rn(a.neg_eps, lse_finish(sj, S));
+    }
+    if (__syncthreads_or(fired) && threadIdx.x == 0) atomicMax(a.guard, k);
   }
 
   __device__ void combine_pairs(float* gnew) {
