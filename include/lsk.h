@@ -211,9 +211,12 @@ int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int3
                                void* stream);
 
 /* cmax_out[b] = max_ij sum_k (x_ik - y_jk)^2 in fp64 (device doubles), the
- * C.max() normaliser of applications.py:186-188, without materialising C. */
+ * C.max() normaliser of applications.py:186-188, without materialising C
+ * (fp32 screen of all pairs, exact fp64 re-evaluation of the near-maximal
+ * ones; d in 1..3). */
+size_t lsk_points_cost_max_workspace_bytes(int32_t B, int32_t n, int32_t m);
 int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
-                            double* cmax_out, void* stream);
+                            double* cmax_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* NCCL communicator for the sharded points solve (one rank per GPU): rank 0
  * gets an id (lsk_nccl_unique_id_bytes() bytes), every rank passes it to

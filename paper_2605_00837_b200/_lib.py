@@ -65,7 +65,8 @@ SIGNATURES = {
     "lsk_points_consume_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_points_consume_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
                                         _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
-    "lsk_points_cost_max": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p]),
+    "lsk_points_cost_max_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
+    "lsk_points_cost_max": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_nccl_unique_id_bytes": (_c_i32, []),
     "lsk_nccl_unique_id": (_c_i32, [_c_p]),
     "lsk_comm_create": (_c_i32, [_c_p, _c_i32, _c_i32, _c_p]),

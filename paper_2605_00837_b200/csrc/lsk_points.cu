@@ -252,8 +252,8 @@ int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_
   P_CUDA(cudaMemsetAsync(rowflag, 0, size_t(B) * (n > m ? n : m) * 4, st));
   P_CUDA(cudaMemsetAsync(nflag, 0, 16, st));
   P_CUDA(cudaMemsetAsync(bad, 0, size_t(B) * 4, st));
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, d, X4);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, d, Y4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, X, n, X4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, X, n, Y4);
   k_pts_init<<<(B + 127) / 128, 128, 0, st>>>(B, S);
   P_CUDA(cudaGetLastError());
 
@@ -280,13 +280,16 @@ int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_
       lsk::k_pts_combine<lsk::kPtsStale><<<g, 256, 0, st>>>(cb);
       P_CUDA(cudaGetLastError());
       if (!h.rpot_new) return LSK_OK;  // check only
-      // guard: rows whose stale sum left [1e-20, 1e30] are recomputed exactly
-      if ((rc = run_part(lsk::kPtsOnline, h, lo, hi, c, act, nullptr, rowflag, nflag))) return rc;
-      lsk::PtsCombine co = cb;
-      co.check = 0;
-      co.nflag_in = nflag;
-      lsk::k_pts_combine<lsk::kPtsOnline><<<g, 256, 0, st>>>(co);
-      P_CUDA(cudaGetLastError());
+      // guard: rows whose stale sum left [1e-20, 1e30] are recomputed exactly by
+      // one CTA per problem (exits at once when nothing was flagged)
+      {
+        lsk::PtsHalf ph{};
+        ph.B = B; ph.n_rows = h.nr; ph.n_cols = h.nc; ph.row_lo = lo; ph.row_hi = hi;
+        ph.rpts = h.rpts; ph.cpts = h.cpts; ph.cpot = h.cpot; ph.clw = h.clw; ph.scale = c.scale;
+        ph.inv_eps = ec.inv; ph.active = act;
+        lsk::k_pts_fixup<<<B, 256, 0, st>>>(ph, ec.neg, h.rpot_new, rowflag, nflag);
+        P_CUDA(cudaGetLastError());
+      }
       P_CUDA(cudaMemsetAsync(nflag, 0, 4, st));
     } else {
       if ((rc = run_part(lsk::kPtsOnline, h, lo, hi, c, act, nullptr, nullptr, nullptr))) return rc;
@@ -399,15 +402,15 @@ int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int3
   float4* part = reinterpret_cast<float4*>(ws);
   ws += al(size_t(B) * chunks * n * 16);
   float2* best = reinterpret_cast<float2*>(ws);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, d, X4);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, d, Y4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, X, n, X4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, X, n, Y4);
   const EpsC ec = epsc(eps);
   lsk::PtsConsume h{B, n, m, chunks, X4, Y4, f, g, log_nu, scale, ec.inv, part, best};
   const int tiles = (n + lsk::kPtsTileRows - 1) / lsk::kPtsTileRows;
   lsk::k_pts_consume<<<dim3(chunks, tiles, B), lsk::kPtsThreads, 0, st>>>(h);
   lsk::k_pts_consume_finish<<<dim3((n + 255) / 256, B), 256, 0, st>>>(B, n, m, d, chunks, part, best, X4, Y4, f, g,
                                                                     log_mu, log_nu, scale, ec.inv, mapped_out,
-                                                                    match_idx, match_w, zero_rows);
+                                                                    match_idx, match_w, zero_rows, X);
   P_CUDA(cudaGetLastError());
   return LSK_OK;
 }
@@ -415,37 +418,39 @@ int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int3
 }  // extern "C"
 
 // Exact fp64 max of sum_k (x_ik - y_jk)^2 per problem (the C.max() normaliser of
-// applications.py:186-188) without materialising C; cmax_out: B device doubles.
-namespace {
-__global__ void k_pts_cmax(const double* __restrict__ X, const double* __restrict__ Y, int n, int m, int d,
-                           unsigned long long* __restrict__ out) {
-  // max over (i, j) of the fp64 direct sum; fp64 >= 0 compares like its bit pattern
-  const int b = blockIdx.y;
-  const double* Xb = X + (size_t)b * n * d;
-  const double* Yb = Y + (size_t)b * m * d;
-  double mx = 0.0;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n * m;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int i = int(idx / m), j = int(idx % m);
-    double acc = 0.0;
-    for (int k = 0; k < d; ++k) {
-      const double t = __dsub_rn(Xb[(size_t)i * d + k], Yb[(size_t)j * d + k]);
-      acc = (k == 0) ? __dmul_rn(t, t) : __dadd_rn(acc, __dmul_rn(t, t));
-    }
-    mx = fmax(mx, acc);
-  }
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out + b, static_cast<unsigned long long>(__double_as_longlong(mx)));
+// applications.py:186-188) without materialising C: an fp32 screen of all
+// pairs on translated points, then exact fp64 re-evaluation of the pairs within
+// 1e-5 of the screened max. The fp32 value of any pair is within ~1e-6
+// relative of its exact value (translation by a data point bounds the rounded
+// coordinates by twice the largest pair distance), so the true maximiser is
+// always among the re-evaluated pairs.
+extern "C" size_t lsk_points_cost_max_workspace_bytes(int32_t B, int32_t n, int32_t m) {
+  if (B < 1 || n < 1 || m < 1) return 0;
+  return al(size_t(B) * n * 16) + al(size_t(B) * m * 16) + al(size_t(B) * 4);
 }
-}  // namespace
 
 extern "C" int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
-                                       double* cmax_out, void* stream) {
+                                       double* cmax_out, void* workspace, size_t workspace_bytes, void* stream) {
   if (!X || !Y || !cmax_out) return pfail(LSK_EINVAL, "null pointer");
   if (B < 1 || n < 1 || m < 1 || d < 1) return pfail(LSK_EINVAL, "bad shape");
+  if (d > 3) return pfail(LSK_EUNSUPPORTED, "points cost max supports d in 1..3");
+  if (!workspace || workspace_bytes < lsk_points_cost_max_workspace_bytes(B, n, m))
+    return pfail(LSK_EINVAL, "workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  float4* X4 = reinterpret_cast<float4*>(ws);
+  ws += al(size_t(B) * n * 16);
+  float4* Y4 = reinterpret_cast<float4*>(ws);
+  ws += al(size_t(B) * m * 16);
+  unsigned* m32 = reinterpret_cast<unsigned*>(ws);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, X, n, X4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, X, n, Y4);
+  P_CUDA(cudaMemsetAsync(m32, 0, size_t(B) * 4, st));
   P_CUDA(cudaMemsetAsync(cmax_out, 0, size_t(B) * 8, st));
-  k_pts_cmax<<<dim3(1184, B), 256, 0, st>>>(X, Y, n, m, d, reinterpret_cast<unsigned long long*>(cmax_out));
+  const dim3 grid(chunks_of(m), (n + lsk::kPtsTileRows - 1) / lsk::kPtsTileRows, B);
+  unsigned long long* m64 = reinterpret_cast<unsigned long long*>(cmax_out);
+  lsk::k_pts_cmax2<0><<<grid, lsk::kPtsThreads, 0, st>>>(n, m, d, X4, Y4, X, Y, m32, m64);
+  lsk::k_pts_cmax2<1><<<grid, lsk::kPtsThreads, 0, st>>>(n, m, d, X4, Y4, X, Y, m32, m64);
   P_CUDA(cudaGetLastError());
   return LSK_OK;
 }

@@ -350,11 +350,18 @@ static __global__ void k_pts_cost_finish(int B, int n, const float* __restrict__
   s.cost = c;
 }
 
-// fp64 points -> float4 (x, y, z, 0) with coordinates beyond d zero
-static __global__ void k_pts_pack(const double* __restrict__ P, long long count, int d, float4* __restrict__ out) {
+// fp64 points -> float4 (x, y, z, 0), coordinates beyond d zero. Each problem
+// is translated by its first source point x_b0 in fp64 before the single fp32
+// rounding: distances are unchanged, and the fp32 coordinates carry the data's
+// spread instead of its offset (the on-the-fly cost stays accurate for clouds
+// far from the origin).
+static __global__ void k_pts_pack(const double* __restrict__ P, long long count, int per_problem, int d,
+                                  const double* __restrict__ X, int n, float4* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / per_problem;
+    const double* c = X + b * (long long)n * d;
     float v[3] = {0.f, 0.f, 0.f};
-    for (int k = 0; k < d; ++k) v[k] = __double2float_rn(P[i * d + k]);
+    for (int k = 0; k < d; ++k) v[k] = __double2float_rn(__dsub_rn(P[i * d + k], c[k]));
     out[i] = make_float4(v[0], v[1], v[2], 0.f);
   }
 }
@@ -468,7 +475,8 @@ static __global__ void k_pts_consume_finish(int B, int n, int m, int d, int chun
                                             const float* __restrict__ g, const float* __restrict__ lmu,
                                             const float* __restrict__ lnu, const float* __restrict__ scale,
                                             float inv_eps, float* __restrict__ mapped, int* __restrict__ idx,
-                                            float* __restrict__ wt, int* __restrict__ zero_rows) {
+                                            float* __restrict__ wt, int* __restrict__ zero_rows,
+                                            const double* __restrict__ X0) {
   const int b = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -484,8 +492,10 @@ static __global__ void k_pts_consume_finish(int B, int n, int m, int d, int chun
   }
   const size_t ri = (size_t)b * n + i;
   if (!(a0 > 0.f)) atomicAdd(zero_rows, 1);  // ZeroRowMass (applications.py:92-93)
+  // undo the translation of k_pts_pack (points were shifted by the problem's first source point)
+  const double* c0 = X0 + (size_t)b * n * d;
   const float out[3] = {a1 / a0, a2 / a0, a3 / a0};
-  for (int k = 0; k < d; ++k) mapped[ri * d + k] = out[k];
+  for (int k = 0; k < d; ++k) mapped[ri * d + k] = __double2float_rn(__dadd_rn(double(out[k]), c0[k]));
   if (j == 0x7fffffff) j = 0;
   idx[ri] = j;
   // pi_ij = exp(((f_i + g_j) - c_ij) * inv + lmu_i + lnu_j), c from the fp32 points
@@ -495,6 +505,115 @@ static __global__ void k_pts_consume_finish(int B, int n, int m, int d, int chun
   const float z = __fadd_rn(__fadd_rn(__fmul_rn(__fsub_rn(__fadd_rn(f[ri], g[(size_t)b * m + j]), c), inv_eps), lmu[ri]),
                             lnu[(size_t)b * m + j]);
   wt[ri] = expf(z);
+}
+
+}  // namespace lsk
+
+namespace lsk {
+
+// Guard fallback without a full-grid launch: one CTA per problem returns
+// at once unless some row's stale sum left the band (nflag > 0, rare); then
+// it recomputes each flagged row exactly -- max pass, then the shifted sum,
+// over all columns in log2 units -- and writes the potential.
+static __global__ void __launch_bounds__(256) k_pts_fixup(PtsHalf h, float neg_eps, float* __restrict__ rpot_new,
+                                                          int* __restrict__ rowflag, int* __restrict__ nflag) {
+  __shared__ float red[64];
+  if (*nflag == 0) return;
+  const int b = blockIdx.x;
+  if (h.active && !h.active[b]) return;
+  const float sc = __ldg(h.scale + b);
+  const float NK = -__fmul_rn(__fmul_rn(h.inv_eps, kLog2e), sc);
+  for (int r = h.row_lo; r < h.row_hi; ++r) {
+    const size_t ri = (size_t)b * h.n_rows + r;
+    if (!rowflag[ri]) continue;  // uniform: every thread reads the same flag
+    const float4 x = h.rpts[ri];
+    auto v_of = [&](int j) {
+      const size_t cj = (size_t)b * h.n_cols + j;
+      const float4 y = h.cpts[cj];
+      const float A = __fmul_rn(__fmaf_rn(h.cpot[cj], h.inv_eps, h.clw[cj]), kLog2e);
+      const float d0 = x.x - y.x, d1 = x.y - y.y, d2 = x.z - y.z;
+      return __fmaf_rn(__fmaf_rn(d2, d2, __fmaf_rn(d1, d1, d0 * d0)), NK, A);
+    };
+    float mx[1] = {-INFINITY};
+    for (int j = threadIdx.x; j < h.n_cols; j += 256) mx[0] = fmax_nan(mx[0], v_of(j));
+    block_reduce<256, 1, true>(mx, red);
+    const float M = mx[0];
+    const float Ms = (fabsf(M) <= 3.402823466e38f) ? M : 0.f;
+    float s[1] = {0.f};
+    for (int j = threadIdx.x; j < h.n_cols; j += 256) s[0] += ex2(v_of(j) - Ms);
+    __syncthreads();
+    block_reduce<256, 1, false>(s, red + 32);
+    if (threadIdx.x == 0) {
+      float L;  // LSE in natural units: M log2-units * ln2 + ln S (reduction.py:196-207)
+      if (!(fabsf(M) <= 3.402823466e38f)) L = -INFINITY;
+      else L = __fadd_rn(__fmul_rn(M, 0.6931471805599453f), logf(fmaxf(s[0], kSumFloor)));
+      rpot_new[ri] = __fmul_rn(neg_eps, L);
+      rowflag[ri] = 0;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace lsk
+
+namespace lsk {
+
+// Exact fp64 max of the squared-Euclidean cost without 2 n m fp64 evaluations:
+// MODE 0 screens all pairs in fp32 (translated points, < 1e-6 relative error,
+// see lsk_points.cu) for max32; MODE 1 re-evaluates in fp64 -- the reference's
+// direct coordinate sum (costs.py:48-49) on the original points -- only the
+// pairs whose fp32 value is within 1e-5 of max32, and keeps their exact max.
+template <int MODE>
+static __global__ void __launch_bounds__(kPtsThreads) k_pts_cmax2(int n, int m, int d, const float4* __restrict__ X4,
+                                                                 const float4* __restrict__ Y4,
+                                                                 const double* __restrict__ X,
+                                                                 const double* __restrict__ Y,
+                                                                 unsigned* __restrict__ max32,
+                                                                 unsigned long long* __restrict__ max64) {
+  __shared__ __align__(16) float4 colv[kPtsChunk];
+  const int ch = blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
+  const int r_base = tile * kPtsTileRows;
+  if (r_base >= n) return;
+  const int j0 = ch * kPtsChunk, ncol = min(kPtsChunk, m - j0);
+  for (int t = threadIdx.x; t < ncol; t += kPtsThreads) colv[t] = Y4[(size_t)b * m + j0 + t];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float x0[8], x1[8], x2[8];
+  int ri[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    int i = r_base + w * kPtsRowsPerWarp + r;
+    ri[r] = i < n ? i : -1;
+    const float4 x = X4[(size_t)b * n + (i < n ? i : n - 1)];
+    x0[r] = x.x; x1[r] = x.y; x2[r] = x.z;
+  }
+  const float T = (MODE == 1) ? __uint_as_float(max32[b]) * (1.0f - 1e-5f) : 0.f;
+  __syncthreads();
+  float mx = 0.f;
+  for (int t = lane; t < ncol; t += 32) {
+    const float4 q = colv[t];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float dx = x0[r] - q.x, dy = x1[r] - q.y, dz = x2[r] - q.z;
+      const float v = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+      if (MODE == 0) {
+        mx = (ri[r] >= 0 && v > mx) ? v : mx;
+      } else if (ri[r] >= 0 && v >= T) {  // rare: exact fp64 re-evaluation
+        const double* xp = X + ((size_t)b * n + ri[r]) * d;
+        const double* yp = Y + ((size_t)b * m + j0 + t) * d;
+        double acc = 0.0;
+        for (int k = 0; k < d; ++k) {
+          const double dd = __dsub_rn(xp[k], yp[k]);
+          acc = (k == 0) ? __dmul_rn(dd, dd) : __dadd_rn(acc, __dmul_rn(dd, dd));
+        }
+        atomicMax(max64 + b, static_cast<unsigned long long>(__double_as_longlong(acc)));
+      }
+    }
+  }
+  if (MODE == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(max32 + b, __float_as_uint(mx));  // non-negative: bits order like values
+  }
 }
 
 }  // namespace lsk

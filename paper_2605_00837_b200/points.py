@@ -66,8 +66,10 @@ def points_cost_max(Xd, Yd):
     B, n, d = Xd.shape
     m = Yd.shape[1]
     out = torch.empty(B, dtype=torch.float64, device="cuda")
-    _lib.call("lsk_points_cost_max", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(out), _stream_ptr(torch))
-    return out
+    wsb = _lib.load().lsk_points_cost_max_workspace_bytes(B, n, m)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.call("lsk_points_cost_max", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(out), _ptr(ws), wsb, _stream_ptr(torch))
+    return out  # ws is freed to the caching allocator in stream order: safe
 
 
 class _PointsRun:

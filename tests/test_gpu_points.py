@@ -116,3 +116,31 @@ def test_points_sharded_one_rank_matches(cuda_ok):
     assert r1.error_trace == r0.error_trace and r1.transport_cost == r0.transport_cost
     np.testing.assert_array_equal(p1.alpha, p0.alpha)
     np.testing.assert_array_equal(p1.beta, p0.beta)
+
+
+def test_points_cost_max_exact(cuda_ok):
+    """The screened max equals the exact fp64 max of the direct sum, including
+    clouds far from the origin and ties."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    cases = [rng.uniform(0, 1, (1, 3000, 3)), rng.uniform(0, 1, (1, 3000, 3)) + 1e4,
+             np.round(rng.uniform(0, 4, (2, 500, 2))), rng.normal(0, 1, (3, 257, 1))]
+    for X in cases:
+        Y = X[:, ::-1].copy() + rng.normal(0, 0.1, X.shape)
+        got = PT.points_cost_max(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()).cpu().numpy()
+        for b in range(X.shape[0]):
+            want = O.sq_euclidean_cost(X[b], Y[b]).max()
+            assert got[b] == want, (got[b], want)
+
+
+def test_points_guard_path_matches_online(cuda_ok):
+    """Small eps on a wide cloud: the stale shift leaves the guard band in
+    early iterations; the per-row exact fixup keeps stale == online."""
+    X, Y = O.uniform_points(600, 2, 11)
+    cfg = lsk.SinkhornConfig(epsilon=3e-4, tolerance=1e-30, max_iterations=15)
+    r1, p1 = PT.solve_points_otf(X * 3, Y * 3, None, None, cfg, stale_shift=True)
+    r2, p2 = PT.solve_points_otf(X * 3, Y * 3, None, None, cfg, stale_shift=False)
+    scale = max(np.abs(p2.alpha).max(), np.abs(p2.beta).max())
+    assert np.abs(p1.alpha - p2.alpha).max() <= 1e-5 * scale
+    assert np.abs(p1.beta - p2.beta).max() <= 1e-5 * scale
