@@ -57,20 +57,21 @@ struct PtsHalf {
 
 __device__ __forceinline__ f2 bc2(float a) { return pk2(a, a); }
 
-// One CTA = one (problem, 64-row tile of the slab, column chunk) unit.
-template <int MODE>
-static __global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
+// One CTA = one (problem, 8*RPW-row tile of the slab, column chunk) unit.
+template <int MODE, int RPW>
+static __global__ void __launch_bounds__(kPtsThreads, (RPW > 8 ? 2 : 3)) k_pts_part(PtsHalf h) {
+  constexpr int PP = RPW / 2, TILE = 8 * RPW;
   __shared__ __align__(16) float4 colv[kPtsChunk];
   __shared__ int tile_any;
   const int ch = blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
   if (MODE == kPtsOnline && h.nflag && *h.nflag == 0) return;
   if (h.active && !h.active[b]) return;
-  const int r_base = h.row_lo + tile * kPtsTileRows;
+  const int r_base = h.row_lo + tile * TILE;
   if (r_base >= h.row_hi) return;
   if (MODE == kPtsOnline && h.rowflag) {
     if (threadIdx.x == 0) tile_any = 0;
     __syncthreads();
-    if (threadIdx.x < kPtsTileRows) {
+    if (threadIdx.x < TILE) {
       const int r = r_base + threadIdx.x;
       if (r < h.row_hi && h.rowflag[(size_t)b * h.n_rows + r]) tile_any = 1;
     }
@@ -91,14 +92,14 @@ static __global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
   }
   // this warp's 8 rows, packed in pairs
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  f2 X0[4], X1[4], X2[4], I0[4];
-  float lrow[8];
+  f2 X0[PP], X1[PP], X2[PP], I0[PP];
+  float lrow[RPW];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
+  for (int p = 0; p < PP; ++p) {
     float xa[3], xb[3], ia, ib;
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
-      int r = r_base + w * kPtsRowsPerWarp + 2 * p + h2;
+      int r = r_base + w * RPW + 2 * p + h2;
       r = r < h.row_hi ? r : h.row_hi - 1;
       const size_t ri = (size_t)b * h.n_rows + r;
       const float4 x = __ldg(h.rpts + ri);
@@ -117,19 +118,19 @@ static __global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
   const f2 NK = bc2(-Kf);
   __syncthreads();
 
-  f2 acc[4];
-  float mx[8], sm[8];
+  f2 acc[PP];
+  float mx[RPW], sm[RPW];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) acc[p] = 0ull;
+  for (int p = 0; p < PP; ++p) acc[p] = 0ull;
 #pragma unroll
-  for (int r = 0; r < 8; ++r) { mx[r] = -INFINITY; sm[r] = 0.f; }
+  for (int r = 0; r < RPW; ++r) { mx[r] = -INFINITY; sm[r] = 0.f; }
 
 #pragma unroll 2
   for (int t = lane; t < ncol; t += 32) {
     const float4 q = colv[t];
     const f2 Q0 = bc2(q.x), Q1 = bc2(q.y), Q2 = bc2(q.z), QA = bc2(q.w);
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
+    for (int p = 0; p < PP; ++p) {
       f2 d = sub2(X0[p], Q0);
       f2 s = (MODE == kPtsCost) ? mul2(d, d) : fma2(d, d, I0[p]);
       d = sub2(X1[p], Q1);
@@ -164,11 +165,11 @@ static __global__ void __launch_bounds__(kPtsThreads, 3) k_pts_part(PtsHalf h) {
   // lane reduction (xor butterfly: fixed order) and store
   const size_t pbase = ((size_t)b * h.chunks + ch) * h.n_rows;
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
+  for (int p = 0; p < PP; ++p) {
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
       const int r8 = 2 * p + h2;
-      const int r = r_base + w * kPtsRowsPerWarp + r8;
+      const int r = r_base + w * RPW + r8;
       if (MODE != kPtsOnline) {
         float a0, a1;
         up2(acc[p], a0, a1);
