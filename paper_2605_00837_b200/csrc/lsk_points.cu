@@ -168,6 +168,7 @@ int32_t run_part(int mode, const Half& h, int lo, int hi, const Ctx& c, const in
   if (tiles <= 0) return LSK_OK;
   dim3 grid(ph.chunks, tiles, c.B);
   if (mode == lsk::kPtsStale) lsk::k_pts_part<lsk::kPtsStale, kWide><<<grid, lsk::kPtsThreads, 0, c.s>>>(ph);
+  else if (mode == lsk::kPtsStaleX) lsk::k_pts_part<lsk::kPtsStaleX, kWide><<<grid, lsk::kPtsThreads, 0, c.s>>>(ph);
   else if (mode == lsk::kPtsOnline) lsk::k_pts_part<lsk::kPtsOnline, 8><<<grid, lsk::kPtsThreads, 0, c.s>>>(ph);
   else lsk::k_pts_part<lsk::kPtsCost, kWide><<<grid, lsk::kPtsThreads, 0, c.s>>>(ph);
   P_CUDA(cudaGetLastError());
@@ -262,6 +263,9 @@ int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_
 
   Ctx c{B, n, m, S, act, ws + L.part, rowflag, nflag, ec.inv, ec.neg, scale, st};
   const bool stale = (flags & LSK_FLAG_STALE_SHIFT) != 0;
+  // expansion-form cost in the stale sweeps: only where its rounding is at the
+  // reference's own level (eps >= 5e-3), and only when asked for
+  const bool expansion = (flags & LSK_FLAG_EXPANSION) != 0 && eps >= 5e-3;
   auto refresh_active = [&]() -> int32_t {
     k_active_view<<<(B + 127) / 128, 128, 0, st>>>(B, S, act);
     P_CUDA(cudaGetLastError());
@@ -273,7 +277,8 @@ int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_
   auto half = [&](const Half& h, int lo, int hi, bool use_stale, bool check, const float* rlw,
                   const float* rmu) -> int32_t {
     if (use_stale) {
-      if ((rc = run_part(lsk::kPtsStale, h, lo, hi, c, act, nullptr, nullptr, nullptr))) return rc;
+      if ((rc = run_part(expansion ? lsk::kPtsStaleX : lsk::kPtsStale, h, lo, hi, c, act, nullptr, nullptr, nullptr)))
+        return rc;
       lsk::PtsCombine cb{};
       cb.B = B; cb.n_rows = h.nr; cb.row_lo = lo; cb.row_hi = hi; cb.chunks = chunks_of(h.nc);
       cb.part = c.part; cb.rpot_old = h.rpot_old; cb.rpot_new = h.rpot_new; cb.inv_eps = ec.inv;

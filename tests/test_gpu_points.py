@@ -30,12 +30,14 @@ def config_of(z):
                               max_iterations=int(z["K"]), check_interval=int(z["check"]))
 
 
-@pytest.mark.parametrize("stale", [True, False], ids=["stale", "online"])
+@pytest.mark.parametrize("variant", ["stale", "online", "expansion"])
 @pytest.mark.parametrize("name", ["rigid2048_eps1e-3_k200", "g5_c5_n4096_rgb_k200", "g1_c1_n1024"])
-def test_points_fixture(cuda_ok, name, stale):
+def test_points_fixture(cuda_ok, name, variant):
     z, X, Y, norm = fixture_points(name)
     rep, pot = PT.solve_points_otf(X, Y, dist(z["mu"]), dist(z["nu"]), config_of(z), normalize=norm,
-                                   stale_shift=stale)
+                                   stale_shift=variant != "online", expansion=variant == "expansion")
+    if variant == "expansion" and float(z["eps"]) < 5e-3:
+        pytest.skip("expansion form only applies at eps >= 5e-3 (direct form ran)")
     assert rep.status == str(z["status"]) and rep.iterations == int(z["iterations"])
     assert [k for k, _ in rep.error_trace] == [int(k) for k in z["trace"][:, 0]]
     # marginal errors: same trajectory within fp32-cost noise

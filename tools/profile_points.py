@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--direct", action="store_true", help="force the direct cost form")
     a = ap.parse_args()
     import torch
 
@@ -44,7 +45,7 @@ def main():
         Ys = np.stack([np.random.Generator(np.random.PCG64(1000 + b)).uniform(0, 1, (4096, 3)) for b in range(a.batch)])
         cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=a.iters)
         for _ in range(a.reps):
-            outs = PT.solve_points_batched(Xs, Ys, cfg)
+            outs = PT.solve_points_batched(Xs, Ys, cfg, expansion=not a.direct)
             dev = outs[0][0].device_seconds
             print(f"c5 B={a.batch} K={a.iters}: device {dev*1e3:.1f} ms = {a.batch * a.iters / dev:.1f} problem-it/s; "
                   f"pairs/s {2 * a.batch * 4096 * 4096 * a.iters / dev:.3e}", flush=True)
