@@ -388,57 +388,28 @@ struct DenseSolver {
         if (CHECK) z += __shfl_xor_sync(0xffffffffu, z, 16 >> l);
       }
   }
-  // after the barrier: finish row i from the warp sums in red[(q&1)]
-  template <bool CHECK>
-  __device__ __forceinline__ float f_finish(const float* row, int q, int i, float fold, float lmu, float* fnew,
-                                            float& err_acc, int& bad) {
-#ifdef LSK_X_NOSUM
-    float M = __fmul_rn(-fold, a.inv_eps), S = red[kRedRows + (q & 1) * NW];
-#else
-    float M = __fmul_rn(-fold, a.inv_eps), S = sum_warps(kRedRows + (q & 1) * NW);
-#endif
-    if (!shift_ok(S)) {  // uniform: every thread holds the same S
-      if (threadIdx.x == 0) atomicAdd(a.stats + 0, 1);
-      exact_row(row, M, S);
-    }
-    // accurate logf: lg2.approx moves f by ~1e-7 relative, which shifts the
-    // marginal error near the fp32 floor enough to flip converged/not_converged
-    // against the reference at err ~ tol (tests: grid64_check5)
-#ifdef LSK_X_NOLOG
-    const float fr = __fmul_rn(a.neg_eps, __fadd_rn(M, S));
-#else
-    const float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
-#endif
-    if (CHECK) check_row(row, i, fold, lmu, sum_warps(kRedRows + 2 * NW + (q & 1) * NW), err_acc, bad);
-    if (threadIdx.x == 0) fnew[i] = fr;
-    return fr;
-  }
-
-  // Step q waits for row q, then finishes row q-1 (sum of the NW warp sums,
-  // accurate logf) in the same straight-line block as row q's row sums, so the
-  // finish's dependency chain overlaps the MUFU stream instead of idling it;
-  // then the column update of row q-1 with row q's butterfly interleaved; one
-  // __syncthreads; the stage of row q-1 is released.
-  // No block barrier per row: each warp posts its row sums with an mbarrier
-  // arrival (SUMS[step & 1]); a warp waits for step q-1's arrivals only when it
-  // needs row q-1's total (at step q). The stage of row q-1 is refilled by the
-  // last warp to finish with it (shared-memory counter). Warps drift by at most
-  // one step, so the double-buffered sums and two barriers suffice.
+  // Row-sum hand-off between warps: no block barrier per row; each warp posts
+  // its row sum with an mbarrier arrival (SUMS[step & 1]) and waits for step
+  // q-1's arrivals only when it needs row q-1's total (at step q).
   __device__ __forceinline__ void post(unsigned step, float s, float z, bool check) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncwarp();  // the warp's reads of the rows it is done with precede the arrival
     if (lane == 0) {
       red[kRedRows + (step & 1) * NW + w] = s;
       if (check) red[kRedRows + 2 * NW + (step & 1) * NW + w] = z;
       mbar_arrive(&bsum[step & 1]);
     }
   }
-  __device__ __forceinline__ void wait_posted(unsigned step) { mbar_wait(&bsum[step & 1], (step >> 1) & 1); }
-  // this warp is done with row (P, q) held in stage st; the last warp to be
-  // done refills the stage with the row STAGES positions later in the sequence
-  __device__ __forceinline__ void release_warp(int st, int P, int q) {
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0 && atom_add_acqrel_smem(&relc[st], 1u) == unsigned(NW - 1)) {
-      relc[st] = 0;
+  __device__ __forceinline__ void wait_posted(unsigned step) {
+#ifndef LSK_X_NOWAIT
+    mbar_wait(&bsum[step & 1], (step >> 1) & 1);
+#endif
+  }
+  // refill the stage that held row (P, q) with the row STAGES positions later
+  // in the sequence (thread 0; every warp is known to be done with it)
+  __device__ __forceinline__ void refill(int st, int P, int q) {
+#ifndef LSK_X_NOTMA
+    if (threadIdx.x == 0) {
       q += STAGES;
       while (q >= rows) { q -= rows; ++P; }
       const uint32_t bytes = uint32_t(a.mpad) * 4u;
@@ -446,22 +417,29 @@ struct DenseSolver {
       mbar_expect_tx(&mbar[st], bytes);
       tma_load_1d(ring + size_t(st) * W, a.C + (long long)row_of(P, q) * a.ldc, bytes, &mbar[st]);
     }
+#endif
   }
-
-  template <bool CHECK>
-  __device__ __forceinline__ float f_finish_async(const float* row, unsigned step, int i, float fold, float lmu,
-                                                  float* fnew, float& err_acc, int& bad) {
-    float M = __fmul_rn(-fold, a.inv_eps), S = sum_warps(kRedRows + (step & 1) * NW);
-    if (!shift_ok(S)) {  // uniform: every thread holds the same S
+  // f of the row whose warp sums are in buffer `buf`: the stale-shift finish is
+  // branch-free so it schedules into the MUFU stream of the next row's sums;
+  // the (rare, CTA-uniform) out-of-range sum falls back to the exact row LSE
+  __device__ __forceinline__ float finish_f(const float* row, float fold, float S) {
+    float M = __fmul_rn(-fold, a.inv_eps);
+    float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
+    if (__builtin_expect(!shift_ok(S), 0)) {
       if (threadIdx.x == 0) atomicAdd(a.stats + 0, 1);
       exact_row(row, M, S);
+      fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
     }
-    const float fr = __fmul_rn(a.neg_eps, lse_finish(M, S));
-    if (CHECK) check_row(row, i, fold, lmu, sum_warps(kRedRows + 2 * NW + (step & 1) * NW), err_acc, bad);
-    if (threadIdx.x == 0) fnew[i] = fr;
     return fr;
   }
 
+  // Step q: wait for row q and for every warp's sums of row q-1 (posted at
+  // step q-1, which also means every warp is done with row q-2: thread 0
+  // refills its stage); then, in one straight-line block, row q's partial sums
+  // and row q-1's finish (sum of the NW warp sums + logf); then the column
+  // update of row q-1 with row q's warp butterfly interleaved; post row q's
+  // warp sum (mbarrier arrival, no block barrier). Warps drift by at most one
+  // step, so two sum buffers / two barriers suffice.
   template <bool CHECK>
   __device__ void fused_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
     const int P = pass++;
@@ -488,7 +466,7 @@ struct DenseSolver {
     if (CHECK) z = warp_sum(z);
     post(g0, s, z, CHECK);
     const float* row_prev = row;
-    int st_prev = st_cur;
+    int st_prev = st_cur, st_pp = 0;
     int i_prev = i_cur;
     float fold_prev = fold_cur, lmu_prev = lmu_cur;
     for (int q = 1; q < rows; ++q) {
@@ -500,26 +478,34 @@ struct DenseSolver {
       }
       st_cur = head_st;
       row = wait_head();
-      // finishing row q-1 next to row q's sums overlaps the logf chain with
-      // the MUFU stream (doing row q's sums first measured 15% slower)
-      wait_posted(g0 + q - 1);
-      const float f_prev = f_finish_async<CHECK>(row_prev, g0 + q - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
+      const unsigned sp = g0 + q - 1;
+      wait_posted(sp);
+      if (q >= 2) refill(st_pp, P, q - 2);
+      const float S = sum_warps(kRedRows + (sp & 1) * NW);
       f_part<CHECK>(row, fold_cur, s, z);
+      const float f_prev = finish_f(row_prev, fold_prev, S);
+      if (CHECK) check_row(row_prev, i_prev, fold_prev, lmu_prev, sum_warps(kRedRows + 2 * NW + (sp & 1) * NW), err_acc, bad);
+      if (threadIdx.x == 0) fnew[i_prev] = f_prev;
       g_part<CHECK, true>(row_prev, f_prev, lmu_prev, s, z);
       carry_f1 = f_prev;
       carry_l1 = lmu_prev;
       post(g0 + q, s, z, CHECK);
-      release_warp(st_prev, P, q - 1);  // this warp is done with row q-1
+      st_pp = st_prev;
       row_prev = row;
       st_prev = st_cur;
       i_prev = i_cur;
       fold_prev = fold_cur;
       lmu_prev = lmu_cur;
     }
-    wait_posted(g0 + rows - 1);
-    const float f_last = f_finish_async<CHECK>(row_prev, g0 + rows - 1, i_prev, fold_prev, lmu_prev, fnew, err_acc, bad);
+    const unsigned sl = g0 + rows - 1;
+    wait_posted(sl);
+    if (rows >= 2) refill(st_pp, P, rows - 2);
+    const float f_last = finish_f(row_prev, fold_prev, sum_warps(kRedRows + (sl & 1) * NW));
+    if (CHECK) check_row(row_prev, i_prev, fold_prev, lmu_prev, sum_warps(kRedRows + 2 * NW + (sl & 1) * NW), err_acc, bad);
+    if (threadIdx.x == 0) fnew[i_prev] = f_last;
     g_part<false, false>(row_prev, f_last, lmu_prev, s, z);
-    release_warp(st_prev, P, rows - 1);
+    __syncthreads();
+    refill(st_prev, P, rows - 1);
     gstep = g0 + rows;
     carry_f0 = f_last;
     carry_l0 = lmu_prev;
@@ -532,7 +518,6 @@ struct DenseSolver {
       iss_step = q2;
       iss_st = head_st;
     }
-    __syncthreads();
   }
   // ================= exact row pass (two-pass max/sum from the on-chip row) ========
   template <bool CHECK>

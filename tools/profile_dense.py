@@ -15,6 +15,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--m", type=int, default=0, help="columns (default n)")
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--eps", type=float, default=1e-3)
     ap.add_argument("--exact", action="store_true")
@@ -28,15 +29,18 @@ def main():
 
     rng = np.random.Generator(np.random.PCG64(0))
     X = rng.uniform(0.0, 1.0, (a.n, 2))
-    Y = rng.uniform(0.0, 1.0, (a.n, 2))
+    m = a.m or a.n
+    Y = rng.uniform(0.0, 1.0, (m, 2))
     C = lsk.squared_euclidean_cost(X, Y)
     w = lsk.make_distribution(np.ones(a.n))
+    wn = lsk.make_distribution(np.ones(m))
     lm = S._dev_f32(torch, w.log_weights)
+    ln = S._dev_f32(torch, wn.log_weights)
     mu = S._dev_f32(torch, w.weights)
     cfg = lsk.SinkhornConfig(epsilon=a.eps, tolerance=1e-30, max_iterations=a.iters)
     ws = None
     for _ in range(a.reps):
-        r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, stale=not a.exact, ws=ws, taskq=a.taskq)
+        r, ws = S._launch_solve(torch, C, lm, ln, mu, cfg, stale=not a.exact, ws=ws, taskq=a.taskq)
     torch.cuda.synchronize()
     print("iters", r.res.cpu().numpy()[:6], "ms", r.ev0.elapsed_time(r.ev1), flush=True)
 
