@@ -227,6 +227,40 @@ int32_t lsk_nccl_unique_id(void* id_out);
 int32_t lsk_comm_create(const void* id, int32_t nranks, int32_t rank, void** comm_out);
 int32_t lsk_comm_destroy(void* comm);
 
+/* ---- colour-transfer pipeline, fp64 (applications.py:100-161)
+ * Replaces: squared_euclidean_cost (costs.py:36-50) in double for the pipeline's
+ * samples; materialize_plan + barycentric_map (solver.py:434-458,
+ * applications.py:75-97) without the plan; the nearest-sample recolour loop
+ * (applications.py:149-155). div != 0 divides every cost by div (the
+ * pipelines' C / C.max()). flags[0] += rows with a non-finite plan entry
+ * (NonFiniteResult), flags[1] += rows with zero mass (ZeroRowMass); flags is
+ * caller-zeroed int32[2]. Recolour: RGB (3 doubles per pixel/sample), ties to
+ * the lowest sample index, output clamped to [0, 1]; nearest may be NULL. */
+int32_t lsk_build_cost_f64(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, double div,
+                           double* C, int64_t ldc, void* stream);
+int32_t lsk_barycentric_points_f64(const double* X, const double* Y, const double* T, int32_t n, int32_t m,
+                                   int32_t d, int32_t dt, double div, const double* log_mu, const double* log_nu,
+                                   const double* alpha, const double* beta, double eps, double* mapped,
+                                   int32_t* flags, void* stream);
+int32_t lsk_recolor_nearest_f64(const double* pixels, int64_t n_pixels, const double* samples, int32_t n_samples,
+                                const double* mapped, double* out, int32_t* nearest, void* stream);
+
+/* ---- standard-domain solve (solver.py:340-431)
+ * K = exp(-C/eps) in the workspace, u = mu/(K v), v = nu/(K^T u) from ones,
+ * checks / trace / cost as lsk_solve_dense_f32 (result[0..2], result_f[0..1]);
+ * mu, nu are the WEIGHTS (not logs). Unguarded by design: non-finite values
+ * surface as status 2 at the next checkpoint. */
+size_t lsk_solve_standard_workspace_bytes(int32_t n, int32_t m, int32_t double_precision);
+int32_t lsk_solve_standard_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* mu, const float* nu,
+                               double eps, double tol, int32_t max_iter, int32_t check, int32_t flags, float* u_out,
+                               float* v_out, int32_t* trace_iter, float* trace_err, int32_t* result, float* result_f,
+                               void* workspace, size_t workspace_bytes, void* stream);
+int32_t lsk_solve_standard_f64(const double* C, int64_t ldc, int32_t n, int32_t m, const double* mu,
+                               const double* nu, double eps, double tol, int32_t max_iter, int32_t check,
+                               int32_t flags, double* u_out, double* v_out, int32_t* trace_iter, double* trace_err,
+                               int32_t* result, double* result_f, void* workspace, size_t workspace_bytes,
+                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,7 @@ the same names, signatures and error behaviour. Kernels live in
 """
 
 from .applications import Correspondence, barycentric_map, match_point_clouds, match_point_clouds_with_report
+from .color import RgbImage, color_transfer, color_transfer_with_report, generate_rigid_pair, make_rgb_image
 from .costs import as_points, solve_points, squared_euclidean_cost
 from .points import solve_points_batched, solve_points_otf
 from .errors import (
@@ -33,6 +34,7 @@ from .solver import (
     update_alpha,
     update_beta,
 )
+from .standard import solve_standard_domain
 from .types import (
     STATUS_CONVERGED,
     STATUS_NOT_CONVERGED,
