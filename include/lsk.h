@@ -231,19 +231,31 @@ int32_t lsk_comm_destroy(void* comm);
  * Replaces: squared_euclidean_cost (costs.py:36-50) in double for the pipeline's
  * samples; materialize_plan + barycentric_map (solver.py:434-458,
  * applications.py:75-97) without the plan; the nearest-sample recolour loop
- * (applications.py:149-155). div != 0 divides every cost by div (the
- * pipelines' C / C.max()). flags[0] += rows with a non-finite plan entry
+ * (applications.py:149-155). lsk_build_cost_f64 takes the arguments of
+ * lsk_build_cost_f32 (normalize_max: C / C.max() when the range is non-zero,
+ * estimator.py:87-89; workspace lsk_build_cost_workspace_bytes()). In the
+ * barycentric map div != 0 divides every recomputed cost by div. flags[0] += rows with a non-finite plan entry
  * (NonFiniteResult), flags[1] += rows with zero mass (ZeroRowMass); flags is
  * caller-zeroed int32[2]. Recolour: RGB (3 doubles per pixel/sample), ties to
  * the lowest sample index, output clamped to [0, 1]; nearest may be NULL. */
-int32_t lsk_build_cost_f64(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, double div,
-                           double* C, int64_t ldc, void* stream);
+int32_t lsk_build_cost_f64(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, int32_t normalize_max,
+                           double* C, int64_t ldc, double* cmax_out, void* workspace, size_t workspace_bytes,
+                           void* stream);
 int32_t lsk_barycentric_points_f64(const double* X, const double* Y, const double* T, int32_t n, int32_t m,
                                    int32_t d, int32_t dt, double div, const double* log_mu, const double* log_nu,
                                    const double* alpha, const double* beta, double eps, double* mapped,
                                    int32_t* flags, void* stream);
 int32_t lsk_recolor_nearest_f64(const double* pixels, int64_t n_pixels, const double* samples, int32_t n_samples,
                                 const double* mapped, double* out, int32_t* nearest, void* stream);
+/* barycentric_map of a materialised (n, m) fp64 plan (applications.py:75-97);
+ * flags[1] += zero-mass rows (ZeroRowMass); dt in 1..4. */
+int32_t lsk_barycentric_plan_f64(const double* P, int64_t ldp, int32_t n, int32_t m, const double* T, int32_t dt,
+                                 double* mapped, int32_t* flags, void* stream);
+/* General nearest-sample map (SinkhornTransport.transform, estimator.py:118-132):
+ * out[q] = mapped[argmin_s |x_q - s|^2] for d = dm in 1..4, optional clamp. */
+int32_t lsk_nearest_map_f64(const double* queries, int64_t n_queries, int32_t d, const double* samples,
+                            int32_t n_samples, const double* mapped, int32_t dm, int32_t clamp01, double* out,
+                            int32_t* nearest, void* stream);
 
 /* ---- standard-domain solve (solver.py:340-431)
  * K = exp(-C/eps) in the workspace, u = mu/(K v), v = nu/(K^T u) from ones,

@@ -34,6 +34,7 @@ from .solver import (
     update_alpha,
     update_beta,
 )
+from .estimator import SinkhornTransport
 from .standard import solve_standard_domain
 from .types import (
     STATUS_CONVERGED,

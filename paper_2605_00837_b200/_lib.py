@@ -68,10 +68,13 @@ SIGNATURES = {
                                         _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_points_cost_max_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_points_cost_max": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
-    "lsk_build_cost_f64": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_dbl, _c_p, _c_i64, _c_p]),
+    "lsk_build_cost_f64": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p, _c_sz,
+                                    _c_p]),
     "lsk_barycentric_points_f64": (_c_i32, [_c_p, _c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_dbl, _c_p, _c_p,
                                             _c_p, _c_p, _c_dbl, _c_p, _c_p, _c_p]),
     "lsk_recolor_nearest_f64": (_c_i32, [_c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_p]),
+    "lsk_barycentric_plan_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p]),
+    "lsk_nearest_map_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_i32, _c_p, _c_i32, _c_i32, _c_p, _c_p, _c_p]),
     "lsk_solve_standard_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_solve_standard_f32": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_dbl, _c_i32, _c_i32,
                                         _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),

@@ -42,19 +42,28 @@ class Correspondence:
 
 def barycentric_map(plan, targets):
     """``mapped_i = sum_j pi_ij t_j / sum_j pi_ij`` for a materialised plan
-    (``applications.py:75-97``); raises ZeroRowMass for an empty row."""
+    (``applications.py:75-97``) in fp64 (``lsk_barycentric_plan_f64``, target
+    coordinates in chunks of up to 4); raises ZeroRowMass for an empty row."""
     torch = _torch()
     T = as_points(targets)
     P = plan.values
     Pt = P if isinstance(P, torch.Tensor) else torch.from_numpy(np.asarray(P))
-    Pt = Pt.to("cuda", torch.float64)
-    if Pt.shape[1] != T.shape[0]:
+    Pt = Pt.to("cuda", torch.float64).contiguous()
+    if Pt.dim() != 2 or Pt.shape[1] != T.shape[0]:
         raise DimensionMismatch(f"plan has {Pt.shape[1]} columns but {T.shape[0]} targets given")
-    denom = Pt.sum(dim=1)
-    if bool((denom == 0).any()):
+    n, m, d = Pt.shape[0], Pt.shape[1], T.shape[1]
+    out = np.empty((n, d), dtype=np.float64)
+    flags = torch.zeros(2, dtype=torch.int32, device="cuda")
+    for k0 in range(0, d, 4):
+        dt = min(4, d - k0)
+        Td = torch.from_numpy(np.ascontiguousarray(T[:, k0:k0 + dt])).to("cuda")
+        mapped = torch.empty((n, dt), dtype=torch.float64, device="cuda")
+        _lib.call("lsk_barycentric_plan_f64", _ptr(Pt), Pt.stride(0), n, m, _ptr(Td), dt, _ptr(mapped), _ptr(flags),
+                  _stream_ptr(torch))
+        out[:, k0:k0 + dt] = mapped.cpu().numpy()
+    if int(flags[1].item()):
         raise ZeroRowMass("a transport plan row has zero total mass")
-    num = Pt @ torch.from_numpy(T).to("cuda")
-    return (num / denom[:, None]).cpu().numpy()
+    return out
 
 
 def _consume(X, Y, pot, eps, normalize, mu=None, nu=None):

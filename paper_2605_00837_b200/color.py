@@ -70,7 +70,7 @@ def color_transfer_with_report(source, target, sample_count, eps, seed):
     S = sample_count
     Xs, Ys = _dev(torch, src_samples), _dev(torch, tgt_samples)
     C = torch.empty((S, S), dtype=torch.float64, device="cuda")
-    _lib.call("lsk_build_cost_f64", _ptr(Xs), _ptr(Ys), S, S, 3, 0.0, _ptr(C), S, st)
+    _lib.call("lsk_build_cost_f64", _ptr(Xs), _ptr(Ys), S, S, 3, 0, _ptr(C), S, None, None, 0, st)
 
     uniform = make_distribution(np.ones(S))
     report, pot = solver64.solve(C, uniform, uniform, SinkhornConfig(epsilon=eps, precision="double"),

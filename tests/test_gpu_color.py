@@ -102,8 +102,14 @@ def test_build_cost_f64_bit_exact(cuda_ok):
     want = ((X[:, None, :] - Y[None, :, :]) ** 2).sum(axis=2)
     Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
     C = torch.empty((70, 91), dtype=torch.float64, device="cuda")
-    _lib.call("lsk_build_cost_f64", Xd.data_ptr(), Yd.data_ptr(), 70, 91, 3, 0.0, C.data_ptr(), 91, None)
+    _lib.call("lsk_build_cost_f64", Xd.data_ptr(), Yd.data_ptr(), 70, 91, 3, 0, C.data_ptr(), 91, None, None, 0, None)
     np.testing.assert_array_equal(C.cpu().numpy(), want)
+    ws = torch.empty(_lib.load().lsk_build_cost_workspace_bytes(), dtype=torch.uint8, device="cuda")
+    cmax = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.call("lsk_build_cost_f64", Xd.data_ptr(), Yd.data_ptr(), 70, 91, 3, 1, C.data_ptr(), 91, cmax.data_ptr(),
+              ws.data_ptr(), ws.numel(), None)
+    assert float(cmax.item()) == want.max()
+    np.testing.assert_array_equal(C.cpu().numpy(), want / want.max())
 
 
 # ---- the reference's TestColorTransfer properties, on this path
