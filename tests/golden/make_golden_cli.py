@@ -43,7 +43,7 @@ def main():
         out[f"nu_{n}_{m}_{seed}"] = nu.weights
         out[f"C_{n}_{m}_{seed}"] = C.values
         out[f"Cn_{n}_{m}_{seed}"] = normalize_cost(C, 10.0).values
-    np.savez_compressed(os.path.join(HERE, "grid_problems.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, "cli_grid_problems.npz"), **out)
 
 
 if __name__ == "__main__":

@@ -49,7 +49,7 @@ def test_usage_errors_exit_2(argv):
 
 
 def test_grid_problems_match_reference():
-    G = golden("grid_problems")
+    G = golden("cli_grid_problems")
     for (n, m, seed) in [(7, 5, 3), (1, 4, 2), (64, 64, 0)]:
         mu, nu, C = generate_grid_problem(n, m, seed)
         np.testing.assert_array_equal(mu.weights, G[f"mu_{n}_{m}_{seed}"])
