@@ -317,6 +317,13 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   return LSK_OK;
 }
 
+#ifdef LSK_X_TRACE
+int32_t lsk_x_read_trace(unsigned long long* out) {
+  LSK_CUDA(cudaMemcpyFromSymbol(out, lsk::lsk_x_trace, sizeof(lsk::lsk_x_trace)));
+  return LSK_OK;
+}
+#endif
+
 int32_t lsk_debug_arg3_f32(const float* a, const float* c, double eps, const float* l, float* out, int32_t count,
                            void* stream) {
   if (!a || !c || !l || !out || count < 2 || (count & 1)) return fail(LSK_EINVAL, "bad debug args");

@@ -70,6 +70,10 @@ struct DenseArgs {
   int* n_trace;
 };
 
+#ifdef LSK_X_TRACE
+__device__ unsigned long long lsk_x_trace[2 * 256 * 3 + 160];
+#endif
+
 template <int NT, int V, int STAGES>
 struct DenseSolver {
   static constexpr int E = 4 * V;       // columns per thread
@@ -477,9 +481,27 @@ struct DenseSolver {
         lmu_nx = __ldg(a.log_mu + i_nx);
       }
       st_cur = head_st;
+#ifdef LSK_X_TRACE
+      const unsigned long long tr0 = clock64();
+#endif
       row = wait_head();
+#ifdef LSK_X_TRACE
+      const unsigned long long tr1 = clock64();
+#endif
       const unsigned sp = g0 + q - 1;
       wait_posted(sp);
+#ifdef LSK_X_TRACE
+      {
+        const unsigned long long tr2 = clock64();
+        const int w = threadIdx.x >> 5;
+        if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (w == 0 || w == NW - 1) && P == 20) {
+          const int k = (w == 0 ? 0 : 1) * 256 + (q & 255);
+          lsk_x_trace[k * 3 + 0] = tr0;
+          lsk_x_trace[k * 3 + 1] = tr1;
+          lsk_x_trace[k * 3 + 2] = tr2;
+        }
+      }
+#endif
       if (q >= 2) refill(st_pp, P, q - 2);
       const float S = sum_warps(kRedRows + (sp & 1) * NW);
       f_part<CHECK>(row, fold_cur, s, z);
@@ -672,14 +694,20 @@ struct DenseSolver {
     bool fired = false;
     if (nc > 0 && QS >= 1 && t < QS * nc) {
       const int c = t % nc, q = t / nc, j = j0 + c;
+      // every partial of the slice in flight at once (one L2 round trip), then
+      // summed in a fixed order
+      constexpr int KB = 24;
       float s = 0.f;
-      int kk = q;
-      for (; kk + 3 * QS < G; kk += 4 * QS) {
-        const float v0 = ldcg(a.part + (size_t)kk * W + j), v1 = ldcg(a.part + (size_t)(kk + QS) * W + j);
-        const float v2 = ldcg(a.part + (size_t)(kk + 2 * QS) * W + j), v3 = ldcg(a.part + (size_t)(kk + 3 * QS) * W + j);
-        s += (v0 + v1) + (v2 + v3);
+      for (int k0 = q; k0 < G; k0 += KB * QS) {
+        float v[KB];
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+          const int kk = k0 + u * QS;
+          v[u] = kk < G ? ldcg(a.part + (size_t)kk * W + j) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < KB; u += 4) s += (v[u] + v[u + 1]) + (v[u + 2] + v[u + 3]);
       }
-      for (; kk < G; kk += QS) s += ldcg(a.part + (size_t)kk * W + j);
       cr[q * nc + c] = s;
     }
     const float gj = (t < nc) ? ldcg(gold + j0 + t) : 0.f;  // issued before the barrier
@@ -780,20 +808,32 @@ struct DenseSolver {
       float err_acc = 0.f;
       int bad = (do_check && gbad) ? 1 : 0;
       const bool fused = a.stale && k > 1;
+#ifdef LSK_X_TRACE
+#define LSK_TR(slot) \
+  if (threadIdx.x == 0 && (b == 0 || b == G - 1) && k >= 20 && k < 30) lsk_x_trace[1536 + (b == 0 ? 0 : 80) + (k - 20) * 8 + (slot)] = clock64()
+#else
+#define LSK_TR(slot)
+#endif
+      LSK_TR(0);
       if (fused) {
         if (do_check) fused_pass<true>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
         else fused_pass<false>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
+        LSK_TR(1);
         store_stale_partials();
       } else {
         if (do_check) row_exact_pass<true>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
         else row_exact_pass<false>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
       }
       if (do_check) publish_check(err_acc, bad);
+      LSK_TR(2);
       grid_barrier(a.bar, epoch);
+      LSK_TR(3);
       if (do_check && decide(k - 1, failed)) { stopped = true; final_k = k - 1; break; }
       if (fused) {
         combine_stale(gcur, gb(k & 1), k);
+        LSK_TR(4);
         grid_barrier(a.bar, epoch);
+        LSK_TR(5);
       }
       const bool need_exact = !fused || (__ldcg(a.guard) == k);
       if (need_exact) {

@@ -122,8 +122,10 @@ __device__ __forceinline__ void block_pair(float (&m)[K], float (&s)[K], float* 
 // LSE finalisation exactly as reduction.py:196-207 given the shift M and the
 // shifted sum S: non-finite M (an all -inf / NaN row) yields -inf.
 __device__ __forceinline__ float lse_finish(float M, float S) {
-  if (!(fabsf(M) <= 3.402823466e38f)) return -INFINITY;
-  return __fadd_rn(M, logf(fmaxf(S, kSumFloor)));
+  // select, not branch: keeps the logf chain in the caller's basic block so it
+  // can be scheduled under independent MUFU work
+  const float r = __fadd_rn(M, logf(fmaxf(S, kSumFloor)));
+  return (fabsf(M) <= 3.402823466e38f) ? r : -INFINITY;
 }
 
 // ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) + mbarrier
@@ -234,6 +236,11 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const unsigned long l
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long atom_add_acqrel64(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
 // Grid barrier on a 64-bit counter: the low word counts arrivals, the high
 // word accumulates a per-CTA flag (e.g. "a guard fired in my rows"), so the
 // barrier also delivers the grid-wide OR without another L2 round trip.
@@ -246,15 +253,16 @@ __device__ __forceinline__ unsigned grid_barrier(unsigned long long* counter, un
   epoch += 1;
   if (threadIdx.x == 0) {
     const unsigned target = epoch * gridDim.x;
-    __threadfence();
-    atomicAdd(counter, 1ull | (static_cast<unsigned long long>(flag) << 32));
-    unsigned long long v = ld_acquire64(counter);
+    // acq_rel add (releases this CTA's writes, ordered before it by the
+    // bar.sync above; acquires when it is the last arrival), else acquire
+    // polling; the trailing bar.sync extends the acquire to the whole CTA
+    unsigned long long v = atom_add_acqrel64(counter, 1ull | (static_cast<unsigned long long>(flag) << 32)) +
+                           (1ull | (static_cast<unsigned long long>(flag) << 32));
     if (static_cast<unsigned>(v) < target) {
       const uint64_t t0 = globaltimer_ns();
       while (static_cast<unsigned>(v = ld_acquire64(counter)) < target)
         if (globaltimer_ns() - t0 > kSpinTimeoutNs) __trap();
     }
-    __threadfence();
     if (scratch) *scratch = static_cast<unsigned>(v >> 32);
   }
   __syncthreads();
