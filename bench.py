@@ -158,7 +158,7 @@ def other_configs():
         cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=tol, max_iterations=K)
         ws = None
         for _ in range(reps):
-            r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, ws=ws)
+            r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, ws=ws, uniform_nu=True)
         torch.cuda.synchronize()
         res = r.res.cpu().numpy()
         sec = r.ev0.elapsed_time(r.ev1) * 1e-3
@@ -279,7 +279,8 @@ def main():
     # ---- device-resident timing: one solve launch per step (stream events)
     wsbuf = None
     for _ in range(args.warmup):
-        r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf)
+        r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf,
+                                       uniform_nu=True)
     torch.cuda.synchronize()
     res = r.res.cpu().numpy()
     assert int(res[1]) == K, res
@@ -291,7 +292,8 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf)
+            r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf,
+                                       uniform_nu=True)
             evs.append((r.ev0, r.ev1))
         e1.record()
         torch.cuda.synchronize()

@@ -54,10 +54,32 @@ using Solver1k = lsk::DenseSolver<256, 1, 16>;
 using Solver2k = lsk::DenseSolver<512, 1, 16>;
 using Solver4k = lsk::DenseSolver<512, 2, 12>;
 using Solver8k = lsk::DenseSolver<512, 4, 6>;
+// uniform target weights (LSK_FLAG_UNIFORM_NU)
+using Solver1kU = lsk::DenseSolver<256, 1, 16, true>;
+using Solver2kU = lsk::DenseSolver<512, 1, 16, true>;
+using Solver4kU = lsk::DenseSolver<512, 2, 12, true>;
+using Solver8kU = lsk::DenseSolver<512, 4, 6, true>;
 
 template <class SV>
 __global__ void __launch_bounds__(SV::NW * 32, 1) k_solve_dense(lsk::DenseArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
+  if constexpr (SV::kUniform) {
+    // the flag's contract, checked by every CTA (so all take the same exit):
+    // a violation ends the solve as numerical_failure after 0 iterations
+    int bad = 0;
+    const float L = __ldg(a.log_nu);
+    for (int j = threadIdx.x; j < a.m; j += blockDim.x) bad |= __ldg(a.log_nu + j) != L;
+    if (__syncthreads_or(bad)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.out_status = 2;
+        *a.out_iters = 0;
+        *a.out_err = NAN;
+        *a.out_cost = NAN;
+        *a.n_trace = 0;
+      }
+      return;
+    }
+  }
   SV sv(a, smem);
   sv.solve();
 }
@@ -298,11 +320,20 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.out_cost = reinterpret_cast<float*>(hdr + 9);
   a.trace_iter = trace_iter;
   a.trace_err = trace_err;
-  switch (L.W) {
-    case 1024: rc = launch_dense<Solver1k>(a, L.G, st); break;
-    case 2048: rc = launch_dense<Solver2k>(a, L.G, st); break;
-    case 4096: rc = launch_dense<Solver4k>(a, L.G, st); break;
-    default: rc = launch_dense<Solver8k>(a, L.G, st); break;
+  if (flags & LSK_FLAG_UNIFORM_NU) {
+    switch (L.W) {
+      case 1024: rc = launch_dense<Solver1kU>(a, L.G, st); break;
+      case 2048: rc = launch_dense<Solver2kU>(a, L.G, st); break;
+      case 4096: rc = launch_dense<Solver4kU>(a, L.G, st); break;
+      default: rc = launch_dense<Solver8kU>(a, L.G, st); break;
+    }
+  } else {
+    switch (L.W) {
+      case 1024: rc = launch_dense<Solver1k>(a, L.G, st); break;
+      case 2048: rc = launch_dense<Solver2k>(a, L.G, st); break;
+      case 4096: rc = launch_dense<Solver4k>(a, L.G, st); break;
+      default: rc = launch_dense<Solver8k>(a, L.G, st); break;
+    }
   }
   if (rc) return rc;
   lsk::k_pick<<<64, 256, 0, st>>>(a.f0, a.f1, a.out_fbuf, n, f_out);

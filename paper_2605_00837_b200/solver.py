@@ -126,7 +126,15 @@ class _Solved:
     __slots__ = ("f", "g", "trace_iter", "trace_err", "res", "resf", "ev0", "ev1")
 
 
-def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None, taskq=False):
+def _uniform(log_w):
+    """All target log-weights equal (host arrays; tensors are not inspected)."""
+    if isinstance(log_w, np.ndarray) and log_w.size:
+        return bool(np.all(log_w.astype(np.float32) == np.float32(log_w[0])))
+    return False
+
+
+def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None, taskq=False,
+                  uniform_nu=False):
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
     cap = _lib.load().lsk_trace_capacity(K, c)
@@ -142,6 +150,7 @@ def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=
     r.resf = torch.zeros(2, dtype=torch.float32, device="cuda")
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
     flags |= _lib.LSK_FLAG_TASKQ if taskq else 0
+    flags |= _lib.LSK_FLAG_UNIFORM_NU if uniform_nu else 0
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
     r.ev0.record()
@@ -211,7 +220,8 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, taskq=
     log_mu = _dev_f32(torch, mu.log_weights)
     log_nu = _dev_f32(torch, nu.log_weights)
     mu32 = _dev_f32(torch, mu.weights)
-    r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift, taskq=taskq)
+    r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift, taskq=taskq,
+                         uniform_nu=_uniform(nu.log_weights))
     return _report_from(r, t0, return_device)
 
 

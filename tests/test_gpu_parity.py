@@ -248,3 +248,32 @@ def test_argument_build_bitwise(cuda_ok):
         _lib.call("lsk_debug_arg3_f32", dev[0].data_ptr(), dev[1].data_ptr(), eps, dev[2].data_ptr(),
                   out.data_ptr(), k, torch.cuda.current_stream().cuda_stream)
         np.testing.assert_array_equal(out.cpu().numpy(), want)
+
+
+def test_uniform_nu_flag_bitwise_and_contract(cuda_ok):
+    """LSK_FLAG_UNIFORM_NU (broadcast log nu) is bit-identical to the general
+    kernel on uniform targets, including padded columns (m % 4 != 0), and a
+    caller that sets it for non-uniform targets gets status 2 after 0 iterations."""
+    import torch
+
+    from paper_2605_00837_b200 import solver as S
+
+    rng = np.random.default_rng(12)
+    for n, m in ((300, 1021), (200, 8190), (64, 3000)):
+        X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+        C = lsk.squared_euclidean_cost(X, Y)
+        mu = lsk.make_distribution(rng.uniform(0.5, 1.5, n))
+        nu = lsk.make_distribution(np.ones(m))
+        cfg = lsk.SinkhornConfig(epsilon=0.01, tolerance=1e-30, max_iterations=60, check_interval=7)
+        lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
+        out = []
+        for uni in (False, True):
+            r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=uni)
+            torch.cuda.synchronize()
+            out.append((r.f.cpu().numpy(), r.g.cpu().numpy(), r.res.cpu().numpy(), r.resf.cpu().numpy()))
+        for a, b in zip(out[0], out[1]):
+            np.testing.assert_array_equal(a, b)
+    nu_bad = lsk.make_distribution(rng.uniform(0.5, 1.5, m))
+    r, _ = S._launch_solve(torch, C, lm, S._dev_f32(torch, nu_bad.log_weights), w, cfg, uniform_nu=True)
+    res = r.res.cpu().numpy()
+    assert res[0] == 2 and res[1] == 0
