@@ -299,6 +299,10 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.max_iter = max_iter; a.check = check_interval;
   a.stale = (flags & LSK_FLAG_STALE_SHIFT) ? 1 : 0;
   a.want_cost = (flags & LSK_FLAG_COST) ? 1 : 0;
+  // multiplicative column update (lsk_dense.cuh, fused_pass_mult): large
+  // problems at eps >= 1e-3 only; its extra rounding is relative to the f-side
+  // argument scale, which only shows on degenerate tiny cases (g == 0 exactly)
+  a.mult = (a.stale && eps >= 1e-3 && (long long)n * m >= (1LL << 20) && !(flags & LSK_FLAG_NO_MULT)) ? 1 : 0;
   a.f0 = reinterpret_cast<float*>(ws + L.off_f0);
   a.f1 = reinterpret_cast<float*>(ws + L.off_f1);
   a.g0 = reinterpret_cast<float*>(ws + L.off_g0);

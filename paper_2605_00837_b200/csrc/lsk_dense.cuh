@@ -47,6 +47,7 @@ struct DenseArgs {
   float negzero;  // -0.0f, passed at run time (see muladd_rn2)
   double tol;
   int max_iter, check, stale, want_cost;
+  int mult;       // column update from the f-side terms (see fused_pass_mult)
   // workspace (zero-initialised by the host where noted)
   float* f0; float* f1;  // f^k lives in f[k & 1]; f0 = 0 on entry
   float* g0; float* g1;  // g^k lives in g[k & 1]; g0 = 0 on entry
@@ -120,7 +121,7 @@ struct DenseSolver {
   f2 g2[P2];   // g_j^{k-1}
   f2 ln2[P2];  // log nu_j (-inf beyond m); unused when UNI
   f2 lnu2;     // UNI: (log nu_0, log nu_0)
-  f2 ns2[P2];  // -fl(fl(-g_j * inv_eps) * log2e): stale column shift, negated
+  float bcol;  // UNI: -log nu_0 * log2 e, the column exponent of fused_pass_mult
   f2 ac2[P2];  // column accumulators
 
   __device__ DenseSolver(const DenseArgs& args, unsigned char* smem) : a(args) {
@@ -215,6 +216,10 @@ struct DenseSolver {
     for (int v = 0; v < V; ++v) lds2x2(base + 4 * (v * NT + threadIdx.x), c[2 * v], c[2 * v + 1]);
   }
 
+  // the stale column shift of g^{k-1}, negated: -fl(fl(-g_j inv_eps) log2 e) =
+  // fl(fl(g_j inv_eps) log2 e) (round-to-nearest is sign-symmetric), formed on
+  // the fly instead of holding 2V more register pairs
+  __device__ __forceinline__ f2 nscol(int p) const { return mul2(mul2(g2[p], inv2), l2e2); }
   __device__ __forceinline__ f2 lnv(int p) const {
     if constexpr (UNI) return lnu2;
     else return ln2[p];
@@ -223,6 +228,7 @@ struct DenseSolver {
     if constexpr (UNI) {
       const float L = __ldg(a.log_nu);
       lnu2 = pk2(L, L);
+      bcol = -__fmul_rn(L, kLog2e);
       return;
     }
 #pragma unroll
@@ -245,18 +251,14 @@ struct DenseSolver {
       const int j0 = col(v, 0);
       float4 t4 = j0 < a.m ? ldcg4(reinterpret_cast<const float4*>(g + j0)) : make_float4(0.f, 0.f, 0.f, 0.f);
       float t[4] = {t4.x, t4.y, t4.z, t4.w};
-      float ns[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (j0 + q >= a.m) t[q] = 0.f;
         bad |= !isfinite(t[q]);
         if (UNI && j0 + q >= a.m) t[q] = -INFINITY;  // padded column: every argument -inf
-        ns[q] = -__fmul_rn(__fmul_rn(-t[q], a.inv_eps), kLog2e);
       }
       g2[2 * v] = pk2(t[0], t[1]);
       g2[2 * v + 1] = pk2(t[2], t[3]);
-      ns2[2 * v] = pk2(ns[0], ns[1]);
-      ns2[2 * v + 1] = pk2(ns[2], ns[3]);
       ac2[2 * v] = 0ull;
       ac2[2 * v + 1] = 0ull;
     }
@@ -391,7 +393,7 @@ struct DenseSolver {
 #pragma unroll
     for (int p = 0; p < P2; ++p) {
 #ifndef LSK_X_NOG
-      ac2[p] = add2(ac2[p], ex2x2(fma2(arg3x2(fi2, c[p], inv2, lm2, nz2), l2e2, ns2[p])));
+      ac2[p] = add2(ac2[p], ex2x2(fma2(arg3x2(fi2, c[p], inv2, lm2, nz2), l2e2, nscol(p))));
 #else
       ac2[p] = add2(ac2[p], c[p]);
 #endif
@@ -556,6 +558,136 @@ struct DenseSolver {
       iss_st = head_st;
     }
   }
+  // ================= fused pass with the multiplicative column update ==============
+  // In exact arithmetic the g-side term of element (i, j) is the f-side term
+  // times 2^(a_i + b_j):  exp(y_ij - M_j) = exp(x_ij - M_i) * exp(a_i + b_j) with
+  // a_i = (f_i^k - f_i^{k-1}) / eps + log mu_i and b_j = -log nu_j (the stale
+  // shifts are M_i = -f^{k-1}_i / eps, M_j = -g^{k-1}_j / eps). So the column
+  // update of row q-1 needs no cost element and no ex2: one FFMA2 per pair
+  // from the f-side terms kept in registers (uniform nu only: b_j is one scalar). It is used for a row
+  // only while a_i stays in a band where no f-side term that underflowed could
+  // matter to a column sum inside the guard band, and only when eps >= 1e-3
+  // (a.mult); otherwise the row takes the direct update. The exponents carry
+  // the f-side argument rounding instead of the g-side one (|dy| <= |y| 2^-24):
+  // parity with the reference stays within the fp32 tolerance at eps >= 1e-3.
+  __device__ __forceinline__ void f_part_e(const float* row, float fold, float& s, f2 (&e)[P2]) const {
+    f2 c[P2];
+    load_row(row, c);
+    const float shl = __fmul_rn(__fmul_rn(-fold, a.inv_eps), kLog2e);
+    const f2 nsl = pk2(-shl, -shl);
+    f2 s2 = 0ull;
+#pragma unroll
+    for (int p = 0; p < P2; ++p) {
+      e[p] = ex2x2(fma2(arg3x2(g2[p], c[p], inv2, lnv(p), nz2), l2e2, nsl));
+      s2 = add2(s2, e[p]);
+    }
+    float s0, s1;
+    up2(s2, s0, s1);
+    s = s0 + s1;
+  }
+  template <bool SHFL>
+  __device__ __forceinline__ void col_update(const float* row, float fi, float fold, float lmu, const f2 (&e)[P2],
+                                             float& s) {
+    const float ai = __fmul_rn(__fadd_rn(__fmul_rn(__fsub_rn(fi, fold), a.inv_eps), lmu), kLog2e);
+    if (ai >= -100.f && ai + bcol <= 23.f) {
+      const float A = ex2(ai + bcol);
+      const f2 A2 = pk2(A, A);
+#pragma unroll
+      for (int p = 0; p < P2; ++p) {
+        ac2[p] = fma2(e[p], A2, ac2[p]);
+        if (SHFL && p < 5) s += __shfl_xor_sync(0xffffffffu, s, 16 >> p);
+      }
+      if (SHFL)
+#pragma unroll
+        for (int l = P2; l < 5; ++l) s += __shfl_xor_sync(0xffffffffu, s, 16 >> l);
+    } else {
+      float z = 0.f;
+      g_part<false, SHFL>(row, fi, lmu, s, z);
+    }
+  }
+
+  __device__ void fused_pass_mult(const float* fprev, float* fnew) {
+    const int P = pass++;
+    int i_cur = row_of(P, 0);
+    int i_nx = rows > 1 ? row_of(P, 1) : i_cur;
+    float fold_cur, lmu_cur, fold_nx, lmu_nx;
+    if (carry_pass == P && rows > 1) {
+      fold_cur = carry_f0; lmu_cur = carry_l0;
+      fold_nx = carry_f1; lmu_nx = carry_l1;
+    } else {
+      fold_cur = ldcg(fprev + i_cur);
+      lmu_cur = __ldg(a.log_mu + i_cur);
+      fold_nx = rows > 1 ? ldcg(fprev + i_nx) : fold_cur;
+      lmu_nx = rows > 1 ? __ldg(a.log_mu + i_nx) : lmu_cur;
+    }
+    const unsigned g0 = gstep;
+    f2 eA[P2], eB[P2];
+    int st_cur = head_st;
+    const float* row = wait_head();
+    float s;
+    f_part_e(row, fold_cur, s, eA);
+    s = warp_sum(s);
+    post(g0, s, 0.f, false);
+    const float* row_prev = row;
+    int st_prev = st_cur, st_pp = 0;
+    int i_prev = i_cur;
+    float fold_prev = fold_cur, lmu_prev = lmu_cur;
+    auto step = [&](int q, const f2 (&ein)[P2], f2 (&eout)[P2]) {
+      i_cur = i_nx; fold_cur = fold_nx; lmu_cur = lmu_nx;
+      if (q + 1 < rows) {
+        i_nx = row_of(P, q + 1);
+        fold_nx = ldcg(fprev + i_nx);
+        lmu_nx = __ldg(a.log_mu + i_nx);
+      }
+      st_cur = head_st;
+      row = wait_head();
+      const unsigned sp = g0 + q - 1;
+      wait_posted(sp);
+      if (q >= 2) refill(st_pp, P, q - 2);
+      const float S = sum_warps(kRedRows + (sp & 1) * NW);
+      f_part_e(row, fold_cur, s, eout);
+      const float f_prev = finish_f(row_prev, fold_prev, S);
+      if (threadIdx.x == 0) fnew[i_prev] = f_prev;
+      col_update<true>(row_prev, f_prev, fold_prev, lmu_prev, ein, s);
+      carry_f1 = f_prev;
+      carry_l1 = lmu_prev;
+      post(g0 + q, s, 0.f, false);
+      st_pp = st_prev;
+      row_prev = row;
+      st_prev = st_cur;
+      i_prev = i_cur;
+      fold_prev = fold_cur;
+      lmu_prev = lmu_cur;
+    };
+    int q = 1;
+    for (; q + 1 < rows; q += 2) {
+      step(q, eA, eB);
+      step(q + 1, eB, eA);
+    }
+    const bool odd = q < rows;
+    if (odd) step(q, eA, eB);
+    const unsigned sl = g0 + rows - 1;
+    wait_posted(sl);
+    if (rows >= 2) refill(st_pp, P, rows - 2);
+    const float f_last = finish_f(row_prev, fold_prev, sum_warps(kRedRows + (sl & 1) * NW));
+    if (threadIdx.x == 0) fnew[i_prev] = f_last;
+    if (odd) col_update<false>(row_prev, f_last, fold_prev, lmu_prev, eB, s);
+    else col_update<false>(row_prev, f_last, fold_prev, lmu_prev, eA, s);
+    __syncthreads();
+    refill(st_prev, P, rows - 1);
+    gstep = g0 + rows;
+    carry_f0 = f_last;
+    carry_l0 = lmu_prev;
+    carry_pass = rows > 1 ? P + 1 : -1;
+    {
+      int q2 = rows + STAGES, P2_ = P;
+      while (q2 >= rows) { q2 -= rows; ++P2_; }
+      iss_pass = P2_;
+      iss_step = q2;
+      iss_st = head_st;
+    }
+  }
+
   // ================= exact row pass (two-pass max/sum from the on-chip row) ========
   template <bool CHECK>
   __device__ void row_exact_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
@@ -832,6 +964,7 @@ struct DenseSolver {
       LSK_TR(0);
       if (fused) {
         if (do_check) fused_pass<true>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
+        else if (UNI && a.mult) fused_pass_mult(fb((k - 1) & 1), fb(k & 1));
         else fused_pass<false>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
         LSK_TR(1);
         store_stale_partials();

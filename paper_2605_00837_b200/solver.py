@@ -134,7 +134,7 @@ def _uniform(log_w):
 
 
 def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None, taskq=False,
-                  uniform_nu=False):
+                  uniform_nu=False, mult=True):
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
     cap = _lib.load().lsk_trace_capacity(K, c)
@@ -151,6 +151,7 @@ def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
     flags |= _lib.LSK_FLAG_TASKQ if taskq else 0
     flags |= _lib.LSK_FLAG_UNIFORM_NU if uniform_nu else 0
+    flags |= 0 if mult else _lib.LSK_FLAG_NO_MULT
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
     r.ev0.record()

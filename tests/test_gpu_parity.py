@@ -268,7 +268,7 @@ def test_uniform_nu_flag_bitwise_and_contract(cuda_ok):
         lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
         out = []
         for uni in (False, True):
-            r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=uni)
+            r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=uni, mult=False)
             torch.cuda.synchronize()
             out.append((r.f.cpu().numpy(), r.g.cpu().numpy(), r.res.cpu().numpy(), r.resf.cpu().numpy()))
         for a, b in zip(out[0], out[1]):
@@ -277,3 +277,29 @@ def test_uniform_nu_flag_bitwise_and_contract(cuda_ok):
     r, _ = S._launch_solve(torch, C, lm, S._dev_f32(torch, nu_bad.log_weights), w, cfg, uniform_nu=True)
     res = r.res.cpu().numpy()
     assert res[0] == 2 and res[1] == 0
+
+
+@pytest.mark.parametrize("n,m,eps", [(8192, 8192, 1e-3), (1024, 1024, 1e-2), (4096, 2048, 2e-3)])
+def test_multiplicative_column_update_close_to_direct(cuda_ok, n, m, eps):
+    """The multiplicative column update (uniform nu, n*m >= 2^20, eps >= 1e-3) against the
+    direct g-side arithmetic on the same problem: potentials within the fp32 parity
+    tolerance, same status and iteration count, cost to 1e-6."""
+    import torch
+
+    from paper_2605_00837_b200 import solver as S
+
+    rng = np.random.default_rng(5)
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, nu = lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(m))
+    cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=300)
+    lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
+    out = []
+    for mult in (False, True):
+        r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=True, mult=mult)
+        torch.cuda.synchronize()
+        out.append((r.f.cpu().numpy(), r.g.cpu().numpy(), r.res.cpu().numpy(), r.resf.cpu().numpy()))
+    (f0, g0, r0, c0), (f1, g1, r1, c1) = out
+    assert r0[0] == r1[0] and r0[1] == r1[1]
+    assert rel_max(f1, f0) <= 1e-5 and rel_max(g1, g0) <= 1e-5, (rel_max(f1, f0), rel_max(g1, g0))
+    assert abs(c1[1] - c0[1]) <= 1e-6 * abs(c0[1])
