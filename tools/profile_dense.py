@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--m", type=int, default=0, help="columns (default n)")
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--eps", type=float, default=1e-3)
+    ap.add_argument("--check", type=int, default=10)
     ap.add_argument("--exact", action="store_true")
     ap.add_argument("--taskq", action="store_true")
     ap.add_argument("--reps", type=int, default=1)
@@ -38,7 +39,7 @@ def main():
     lm = S._dev_f32(torch, w.log_weights)
     ln = S._dev_f32(torch, wn.log_weights)
     mu = S._dev_f32(torch, w.weights)
-    cfg = lsk.SinkhornConfig(epsilon=a.eps, tolerance=1e-30, max_iterations=a.iters)
+    cfg = lsk.SinkhornConfig(epsilon=a.eps, tolerance=1e-30, max_iterations=a.iters, check_interval=a.check)
     ws = None
     for _ in range(a.reps):
         r, ws = S._launch_solve(torch, C, lm, ln, mu, cfg, stale=not a.exact, ws=ws, taskq=a.taskq,

@@ -27,7 +27,7 @@ def main():
     w, wn = lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(8192))
     lm, ln, mu = S._dev_f32(torch, w.log_weights), S._dev_f32(torch, wn.log_weights), S._dev_f32(torch, w.weights)
     cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=40)
-    S._launch_solve(torch, C, lm, ln, mu, cfg)
+    S._launch_solve(torch, C, lm, ln, mu, cfg, uniform_nu=True)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (2 * 256 * 3 + 160))()
     _lib.load().lsk_x_read_trace(buf)
