@@ -310,3 +310,32 @@ def test_multiplicative_column_update_close_to_direct(cuda_ok, n, m, eps):
     assert r0[0] == r1[0] and r0[1] == r1[1]
     assert rel_max(f1, f0) <= 1e-5 and rel_max(g1, g0) <= 1e-5, (rel_max(f1, f0), rel_max(g1, g0))
     assert abs(c1[1] - c0[1]) <= 1e-6 * abs(c0[1])
+
+
+@pytest.mark.parametrize("n,m,eps", [(1, 8192, 1e-3), (149, 4097, 2e-3), (5000, 8191, 1e-3), (20000, 6000, 5e-3),
+                                     (300, 8192, 1e-4)])
+def test_uniform_kernel_shapes_vs_general(cuda_ok, n, m, eps):
+    """The uniform-target kernel (8 warps x 32 columns beyond m = 4096, multiplicative column
+    update where it applies) against the general kernel on awkward shapes: one row, one or two
+    rows per CTA, heavy column padding, hundreds of rows per CTA, and eps below the
+    multiplicative gate."""
+    import torch
+
+    from paper_2605_00837_b200 import solver as S
+
+    rng = np.random.default_rng(n + m)
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, nu = lsk.make_distribution(rng.uniform(0.5, 1.5, n)), lsk.make_distribution(np.ones(m))
+    cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=40, check_interval=10)
+    lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
+    out = []
+    for uni in (False, True):
+        r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=uni)
+        torch.cuda.synchronize()
+        out.append((r.f.cpu().numpy(), r.g.cpu().numpy(), r.res.cpu().numpy(), r.resf.cpu().numpy()))
+    (f0, g0, r0, c0), (f1, g1, r1, c1) = out
+    assert r0[0] == r1[0] and r0[1] == r1[1]
+    assert np.isfinite(f1).all() and np.isfinite(g1).all()
+    assert rel_max(f1, f0) <= 1e-5 and rel_max(g1, g0) <= 1e-5, (rel_max(f1, f0), rel_max(g1, g0))
+    assert abs(c1[1] - c0[1]) <= 1e-5 * abs(c0[1])
