@@ -51,6 +51,16 @@ template <> __device__ __forceinline__ double ddiv(double a, double b) { return 
 __device__ __forceinline__ float dexp(float x) { return expf(x); }
 __device__ __forceinline__ double dexp(double x) { return exp(x); }
 
+// 4 consecutive values (16-byte aligned for float, 2 x 16 B for double)
+__device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
+  const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+
 template <class T>
 __device__ __forceinline__ T warp_sum_t(T v) {
 #pragma unroll
@@ -79,7 +89,9 @@ __global__ void k_gibbs(const T* __restrict__ C, long long ldc, int n, int m, T 
       Kmat[(long long)i * ldk + j] = dexp(ddiv(-C[(long long)i * ldc + j], eps));
 }
 
-// MODE 0: u_i = mu_i / (K v)_i.  MODE 1: term_i = |u_i (K v)_i - mu_i| (check)
+// MODE 0: u_i = mu_i / (K v)_i.  MODE 1: term_i = |u_i (K v)_i - mu_i| (check).
+// One CTA per row, 4 consecutive columns per thread per step (vector loads),
+// fixed-order block sum.
 template <class T, int MODE>
 __global__ void __launch_bounds__(256) k_rowdot(const T* __restrict__ Kmat, long long ldk, int n, int m,
                                                 const T* __restrict__ v, const T* __restrict__ mu,
@@ -90,7 +102,18 @@ __global__ void __launch_bounds__(256) k_rowdot(const T* __restrict__ Kmat, long
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const T* row = Kmat + (long long)i * ldk;
     T s = T(0);
-    for (int j = threadIdx.x; j < m; j += blockDim.x) s = dadd(s, dmul(row[j], v[j]));
+    for (int j = 4 * threadIdx.x; j < m; j += 4 * blockDim.x) {
+      if (j + 3 < m) {
+        T k[4], w[4];
+        ld4(row + j, k);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[c] = v[j + c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s = dadd(s, dmul(k[c], w[c]));
+      } else {
+        for (int c = 0; j + c < m; ++c) s = dadd(s, dmul(row[j + c], v[j + c]));
+      }
+    }
     s = block_sum_t(s, sh);
     if (threadIdx.x == 0) {
       if (MODE == 0) u[i] = ddiv(mu[i], s);
@@ -100,24 +123,40 @@ __global__ void __launch_bounds__(256) k_rowdot(const T* __restrict__ Kmat, long
   }
 }
 
-// column partials over row slabs of rs rows: part[p][j] = sum_{i in slab p} K_ij u_i
+// column partials over row slabs of rs rows: part[p][j] = sum_{i in slab p} K_ij u_i;
+// 4 columns per thread, 8 rows of vector loads in flight
 template <class T>
 __global__ void __launch_bounds__(256) k_colpart(const T* __restrict__ Kmat, long long ldk, int n, int m,
                                                  const T* __restrict__ u, int rs, T* __restrict__ part,
                                                  const int* __restrict__ act) {
   if (act && !*act) return;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= m) return;
+  const int j0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (j0 >= m) return;
   const int i0 = blockIdx.y * rs, i1 = min(n, i0 + rs);
-  T s = T(0);
+  T s[4] = {T(0), T(0), T(0), T(0)};
   int i = i0;
-  for (; i + 3 < i1; i += 4) {
-    const T a = dmul(Kmat[(long long)i * ldk + j], u[i]), b = dmul(Kmat[(long long)(i + 1) * ldk + j], u[i + 1]);
-    const T c = dmul(Kmat[(long long)(i + 2) * ldk + j], u[i + 2]), d = dmul(Kmat[(long long)(i + 3) * ldk + j], u[i + 3]);
-    s = dadd(s, dadd(dadd(a, b), dadd(c, d)));
+  for (; i + 7 < i1; i += 8) {
+    T k[8][4], uu[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      ld4(Kmat + (long long)(i + r) * ldk + j0, k[r]);
+      uu[r] = u[i + r];
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[c] = dadd(s[c], dmul(k[r][c], uu[r]));
   }
-  for (; i < i1; ++i) s = dadd(s, dmul(Kmat[(long long)i * ldk + j], u[i]));
-  part[(long long)blockIdx.y * m + j] = s;
+  for (; i < i1; ++i) {
+    T k[4];
+    ld4(Kmat + (long long)i * ldk + j0, k);
+    const T ui = u[i];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s[c] = dadd(s[c], dmul(k[c], ui));
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (j0 + c < m) part[(long long)blockIdx.y * m + j0 + c] = s[c];
 }
 
 template <class T>
@@ -245,7 +284,7 @@ int num_sms_s() {
   return sms > 0 ? sms : 148;
 }
 int std_parts(int n, int m, int* rs_out) {
-  const int tiles = (m + 255) / 256;
+  const int tiles = (m + 1023) / 1024;
   const int want = (4 * num_sms_s() + tiles - 1) / tiles;
   int rs = (n + want - 1) / want;
   if (rs < 32) rs = 32;
@@ -319,7 +358,7 @@ int32_t solve_standard(const T* C, int64_t ldc, int32_t n, int32_t m, const T* m
   int32_t rc;
   for (int k = 1; k <= K; ++k) {
     k_rowdot<T, 0><<<rblocks, 256, 0, st>>>(Km, L.ldk, n, m, v, mu, u, nullptr, act);
-    k_colpart<T><<<dim3((m + 255) / 256, parts), 256, 0, st>>>(Km, L.ldk, n, m, u, rs, part, act);
+    k_colpart<T><<<dim3((m + 1023) / 1024, parts), 256, 0, st>>>(Km, L.ldk, n, m, u, rs, part, act);
     k_colfin<T><<<(m + 255) / 256, 256, 0, st>>>(part, parts, m, nu, v, act);
     S_CUDA(cudaGetLastError());
     if (k % c == 0 && k < K && (rc = check(k, false))) return rc;
