@@ -262,6 +262,36 @@ int32_t lsk_nearest_map_f64(const double* queries, int64_t n_queries, int32_t d,
                             int32_t n_samples, const double* mapped, int32_t dm, int32_t clamp01, double* out,
                             int32_t* nearest, void* stream);
 
+/* ---- the reference's deterministic reductions (reduction.py)
+ * op: 0 max, 1 sum, 2 log-sum-exp; dtype: 0 float32, 1 float64. Rows: A is (R, L)
+ * with row stride lda, one result per row. Cols: A is (L, R) with row stride lda,
+ * one result per column. The ReductionPlan tree (lane fold over group_size lanes,
+ * ceil-halving within chunk_width chunks, then across chunks) is replicated
+ * exactly: max and sum are bit-identical to the reference; LSE (workspace
+ * lsk_reduce_workspace_bytes(R, dtype)) matches to the exponential's ulps.
+ * group_size <= 4096 (rows), <= 200 KB / (32 * sizeof) (cols). */
+size_t lsk_reduce_workspace_bytes(int32_t R, int32_t dtype);
+int32_t lsk_reduce_rows(const void* A, int64_t lda, int32_t R, int32_t L, int32_t dtype, int32_t op,
+                        int32_t chunk_width, int32_t group_size, void* out, void* workspace, size_t workspace_bytes,
+                        void* stream);
+int32_t lsk_reduce_cols(const void* A, int64_t lda, int32_t L, int32_t R, int32_t dtype, int32_t op,
+                        int32_t chunk_width, int32_t group_size, void* out, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* ---- plan diagnostics (solver.py:461-519)
+ * lsk_kkt_residual: out_max = max |C + eps log(P/(mu nu)) - alpha - beta| over
+ * P >= tiny(dtype) (0 if none), out_count[0] = masked entries, out_count[1] = 1
+ * if a masked residual was NaN; C, P, mu, nu, alpha, beta in dtype (0 f32,
+ * 1 f64), C and P with the same row stride ld; workspace 16 bytes.
+ * lsk_regularized_objective_f64: <C,P> + eps (sum P (log(P/(mu nu)) - 1) + 1),
+ * zero entries contributing 0; workspace 16 n bytes. */
+int32_t lsk_kkt_residual(const void* C, const void* P, int64_t ld, int32_t n, int32_t m, const void* mu,
+                         const void* nu, const void* alpha, const void* beta, double eps, int32_t dtype,
+                         double* out_max, int32_t* out_count, void* workspace, size_t workspace_bytes, void* stream);
+int32_t lsk_regularized_objective_f64(const double* C, const double* P, int64_t ld, int32_t n, int32_t m,
+                                      const double* mu, const double* nu, double eps, double* out, void* workspace,
+                                      size_t workspace_bytes, void* stream);
+
 /* ---- standard-domain solve (solver.py:340-431)
  * K = exp(-C/eps) in the workspace, u = mu/(K v), v = nu/(K^T u) from ones,
  * checks / trace / cost as lsk_solve_dense_f32 (result[0..2], result_f[0..1]);

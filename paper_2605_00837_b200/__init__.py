@@ -34,7 +34,21 @@ from .solver import (
     update_alpha,
     update_beta,
 )
+from .diagnostics import contraction_rate_bound, kkt_residual, regularized_objective
 from .estimator import SinkhornTransport
+from .fileio import read_correspondences, read_point_cloud, read_ppm, write_correspondences, write_point_cloud, write_ppm
+from .problems import generate_grid_problem, normalize_cost
+from .reduction import (
+    log_sum_exp,
+    log_sum_exp_cols,
+    log_sum_exp_rows,
+    reduce_max,
+    reduce_max_cols,
+    reduce_max_rows,
+    reduce_sum,
+    reduce_sum_cols,
+    reduce_sum_rows,
+)
 from .standard import solve_standard_domain
 from .types import (
     STATUS_CONVERGED,

@@ -77,6 +77,13 @@ SIGNATURES = {
     "lsk_recolor_nearest_f64": (_c_i32, [_c_p, _c_i64, _c_p, _c_i32, _c_p, _c_p, _c_p, _c_p]),
     "lsk_barycentric_plan_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_i32, _c_p, _c_p, _c_p]),
     "lsk_nearest_map_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_p, _c_i32, _c_p, _c_i32, _c_i32, _c_p, _c_p, _c_p]),
+    "lsk_kkt_residual": (_c_i32, [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl, _c_i32, _c_p,
+                                  _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_regularized_objective_f64": (_c_i32, [_c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_p, _c_p,
+                                               _c_sz, _c_p]),
+    "lsk_reduce_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
+    "lsk_reduce_rows": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_reduce_cols": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_solve_standard_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_solve_standard_f32": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl, _c_dbl, _c_i32, _c_i32,
                                         _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
