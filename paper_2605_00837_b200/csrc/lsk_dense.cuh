@@ -113,6 +113,7 @@ struct DenseSolver {
   // consumers wait rows in the same order (head) and release them in order (tail).
   int iss_st, iss_pass, iss_step;  // next row to issue
   int head_st, head_ph;            // next row to wait for
+  bool head_ready;                 // a probe saw the next row's TMA complete
   unsigned epoch;
   int pass;                        // pass counter (sweep direction = pass & 1)
   f2 inv2, l2e2, nz2;
@@ -139,6 +140,7 @@ struct DenseSolver {
     rows = r1 - r0;
     iss_st = iss_pass = iss_step = 0;
     head_st = head_ph = 0;
+    head_ready = false;
     epoch = 0;
     pass = 0;
     inv2 = pk2(a.inv_eps, a.inv_eps);
@@ -189,11 +191,19 @@ struct DenseSolver {
   // wait for the next row of the sequence; returns its smem copy
   __device__ __forceinline__ const float* wait_head() {
 #ifndef LSK_X_NOTMA
-    mbar_wait(&mbar[head_st], uint32_t(head_ph));
+    if (!head_ready) mbar_wait(&mbar[head_st], uint32_t(head_ph));
 #endif
+    head_ready = false;
     const float* p = ring + size_t(head_st) * W;
     if (++head_st == STAGES) { head_st = 0; head_ph ^= 1; }
     return p;
+  }
+  // probe the next row's TMA now so the next wait_head can skip the blocking
+  // wait (the mbarrier round trip then overlaps this step's math)
+  __device__ __forceinline__ void probe_head() {
+#ifndef LSK_X_NOTMA
+    head_ready = mbar_test(smem_u32(&mbar[head_st]), uint32_t(head_ph));
+#endif
   }
   // release the oldest held row (call after a __syncthreads that follows every
   // read of it) and refill its stage with the next row of the sequence
@@ -624,6 +634,7 @@ struct DenseSolver {
     f2 eA[P2], eB[P2];
     int st_cur = head_st;
     const float* row = wait_head();
+    probe_head();
     float s;
     f_part_e(row, fold_cur, s, eA);
     s = warp_sum(s);
@@ -641,6 +652,7 @@ struct DenseSolver {
       }
       st_cur = head_st;
       row = wait_head();
+      probe_head();
       const unsigned sp = g0 + q - 1;
       wait_posted(sp);
       if (q >= 2) refill(st_pp, P, q - 2);

@@ -155,6 +155,20 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // is a bug (lost TMA bytes, a CTA that never arrives); trap instead of hanging.
 constexpr uint64_t kSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
+// non-blocking probe of a phase (acquire semantics when it returns true)
+__device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
