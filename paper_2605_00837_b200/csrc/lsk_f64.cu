@@ -126,6 +126,12 @@ __global__ void __launch_bounds__(256) k_col_pairs_d(const double* __restrict__ 
   double M = -INFINITY, S = 0.0;
   for (int i = i0; i < i1; ++i) {
     const double y = arg3d(alpha[i], C[(long long)i * ldc + j], inv, lmu[i]);
+    if (y <= M && fabs(M) <= 1.7976931348623157e308) {
+      // max unchanged: the general update's rescale is exp(0) = 1 exactly, so
+      // skipping it gives the same bits for one exp instead of two
+      S = S + exp(__dsub_rn(y, M));
+      continue;
+    }
     const double mn = dmax_nan(M, y);
     const double ms = (fabs(mn) <= 1.7976931348623157e308) ? mn : 0.0;
     S = (M == -INFINITY ? 0.0 : S * exp(__dsub_rn(M, ms))) + exp(__dsub_rn(y, ms));
