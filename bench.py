@@ -187,6 +187,9 @@ def other_configs():
                  "iters_per_s": v, "guard_stats": res[4:6].tolist(),
                  "time_to_tolerance": time_to_tol(8192, 1e-4, 30000, [1e-6])}
     out["C2_time_to_tolerance"] = time_to_tol(8192, 1e-3, 20000, [1e-6, 1e-5])
+    # the paper's headline shape (n=m=8192, eps=1e-2, solve to the default tolerance); the paper
+    # reports 371.6 ms for 82 iterations on an RTX 3090 (its problem law is unstated)
+    out["paper_shape_eps1e-2_to_tol"] = time_to_tol(8192, 1e-2, 10000, [1e-6])
     # C4: rigid pair n=m=65536 3-D, C/C.max(), eps=1e-3, on the fly, 1 GPU
     n, K = 65536, 20
     rng = np.random.Generator(np.random.PCG64(0))
