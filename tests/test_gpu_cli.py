@@ -66,3 +66,14 @@ def test_cli_color_transfer_and_pointcloud(cuda_ok, tmp_path):
     rc, recs = run(["pointcloud", "--n", "100", "--eps", "0.01", "--out-pairs", str(tmp_path / "p.txt"), "--json"])
     assert rc == 0 and recs[0].status in ("converged", "diverged")
     assert len(fileio.read_correspondences(tmp_path / "p.txt")) == 100
+
+
+def test_cli_worker_count_invariance(cuda_ok):
+    """Reference acceptance criterion 10 / test_cli.py:297-323: records are identical
+    (except the two elapsed columns) for --parallel-experiments 1 and 4, and across runs."""
+    argv = ["stability", "--n", "48", "--eps-grid", "0.1,0.01", "--maxc-grid", "1,10", "--max-iters", "200",
+            "--json"]
+    runs = [run(argv + ["--parallel-experiments", str(k)])[1] for k in (1, 4, 1)]
+    strip = lambda recs: [{f: getattr(r, f) for f in cli.CSV_HEADER if not f.startswith("elapsed")} for r in recs]
+    a, b, c = (strip(r) for r in runs)
+    assert a == b == c
