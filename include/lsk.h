@@ -43,6 +43,8 @@ extern "C" {
 #define LSK_FLAG_EXPANSION 8   /* points, eps >= 5e-3: cost as |x|^2+|y|^2-2x.y in the stale sweeps */
 #define LSK_FLAG_NO_MULT 32    /* dense m <= 8192, uniform nu, n*m >= 2^20, eps >= 1e-3: disable the
                                   multiplicative column update (g-side terms from the f-side ones) */
+#define LSK_FLAG_STD_MULTIKERNEL 64 /* standard domain: force the two-pass multi-kernel loop (fp32 m <= 8192
+                                       otherwise runs the one-pass persistent kernel) */
 #define LSK_FLAG_UNIFORM_NU 16 /* dense m <= 8192: caller asserts log_nu[j] == log_nu[0] for all j (uniform
                                   target weights); the kernel verifies it and a violation ends the solve as
                                   status 2 after 0 iterations */

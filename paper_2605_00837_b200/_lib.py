@@ -23,6 +23,7 @@ LSK_FLAG_TASKQ = 4
 LSK_FLAG_EXPANSION = 8
 LSK_FLAG_UNIFORM_NU = 16
 LSK_FLAG_NO_MULT = 32
+LSK_FLAG_STD_MULTIKERNEL = 64
 
 _c_i32, _c_i64, _c_sz, _c_dbl, _c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_double, ctypes.c_void_p
 

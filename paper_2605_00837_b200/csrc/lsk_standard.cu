@@ -17,7 +17,10 @@
 #include <cmath>
 #include <string>
 
+#include <type_traits>
+
 #include "../../include/lsk.h"
+#include "lsk_stdfused.cuh"
 
 namespace lsk_host {
 int32_t fail(int32_t code, const std::string& msg);
@@ -81,12 +84,14 @@ __device__ __forceinline__ T block_sum_t(T v, T* sh) {
   return r;  // valid in thread 0
 }
 
+// K = exp(-C / eps); the row padding [m, ldk) is written as 0 (the one-pass
+// kernel copies whole 16-byte groups and multiplies them by v = 0 there)
 template <class T>
 __global__ void k_gibbs(const T* __restrict__ C, long long ldc, int n, int m, T eps, T* __restrict__ Kmat,
                         long long ldk) {
   for (int i = blockIdx.y; i < n; i += gridDim.y)
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x)
-      Kmat[(long long)i * ldk + j] = dexp(ddiv(-C[(long long)i * ldc + j], eps));
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ldk; j += gridDim.x * blockDim.x)
+      Kmat[(long long)i * ldk + j] = j < m ? dexp(ddiv(-C[(long long)i * ldc + j], eps)) : T(0);
 }
 
 // MODE 0: u_i = mu_i / (K v)_i.  MODE 1: term_i = |u_i (K v)_i - mu_i| (check).
@@ -294,8 +299,12 @@ int std_parts(int n, int m, int* rs_out) {
 
 struct StdLayout {
   size_t K, part, term, blk, bad, state, act, total;
+  // fused one-pass path (fp32, m <= 8192)
+  size_t u0, u1, v0, v1, fpart, errp, flagp, bar, outbuf;
   long long ldk;
 };
+using StdFused = lsk::StdSolver<512, 4, 6>;
+constexpr int kStdW = StdFused::W;
 template <class T>
 StdLayout std_layout(int n, int m) {
   StdLayout L{};
@@ -310,8 +319,42 @@ StdLayout std_layout(int n, int m) {
   L.bad = o; o = al(o + 16);
   L.state = o; o = al(o + sizeof(StdState<T>));
   L.act = o; o = al(o + 16);
+  if (sizeof(T) == 4 && m <= kStdW) {
+    const int G = num_sms_s();
+    L.u0 = o; o = al(o + size_t(n) * 4);
+    L.u1 = o; o = al(o + size_t(n) * 4);
+    L.v0 = o; o = al(o + size_t(kStdW) * 4);
+    L.v1 = o; o = al(o + size_t(kStdW) * 4);
+    L.fpart = o; o = al(o + size_t(G) * kStdW * 4);
+    L.errp = o; o = al(o + size_t(G) * 4);
+    L.flagp = o; o = al(o + size_t(G) * 4);
+    L.bar = o; o = al(o + 16);
+    L.outbuf = o; o = al(o + 16);
+  }
   L.total = o;
   return L;
+}
+
+__global__ void k_std_fused(lsk::StdArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  StdFused sv(a, smem);
+  sv.solve();
+}
+__global__ void k_std_init(float* u0, int n, float* v0, int m, StdState<float>* st) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int i = t; i < n; i += gridDim.x * blockDim.x) u0[i] = 1.f;
+  for (int j = t; j < kStdW; j += gridDim.x * blockDim.x) v0[j] = j < m ? 1.f : 0.f;
+  if (t == 0) {
+    StdState<float> s{};
+    s.active = 1;
+    *st = s;
+  }
+}
+__global__ void k_std_pick(const float* u0, const float* u1, int n, const float* v0, const float* v1, int m,
+                           const int* outbuf, float* u, float* v) {
+  const int sel = *outbuf;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) u[i] = sel ? u1[i] : u0[i];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) v[j] = sel ? v1[j] : v0[j];
 }
 
 template <class T>
@@ -346,6 +389,44 @@ int32_t solve_standard(const T* C, int64_t ldc, int32_t n, int32_t m, const T* m
   int bx = (m + 255) / 256;
   if (bx > 32) bx = 32;
   k_gibbs<T><<<dim3(bx, n < 65535 ? n : 65535), 256, 0, st>>>(C, ldc, n, m, T(eps), Km, L.ldk);
+  if constexpr (std::is_same<T, float>::value) {
+    if (m <= kStdW && !(flags & LSK_FLAG_STD_MULTIKERNEL)) {
+      // one persistent launch, one read of K per iteration (lsk_stdfused.cuh)
+      const int G = num_sms_s() < n ? num_sms_s() : n;
+      lsk::StdArgs sa{};
+      sa.K = Km; sa.ldk = L.ldk; sa.n = n; sa.m = m; sa.mpad = (m + 3) / 4 * 4;
+      sa.mu = mu; sa.nu = nu; sa.tol = tol; sa.max_iter = K; sa.check = c;
+      sa.u0 = reinterpret_cast<float*>(ws + L.u0); sa.u1 = reinterpret_cast<float*>(ws + L.u1);
+      sa.v0 = reinterpret_cast<float*>(ws + L.v0); sa.v1 = reinterpret_cast<float*>(ws + L.v1);
+      sa.part = reinterpret_cast<float*>(ws + L.fpart);
+      sa.errpart = reinterpret_cast<float*>(ws + L.errp);
+      sa.flagpart = reinterpret_cast<int*>(ws + L.flagp);
+      sa.bar = reinterpret_cast<unsigned long long*>(ws + L.bar);
+      sa.st_active = &S->active; sa.st_status = &S->status; sa.st_iters = &S->iters; sa.st_ntrace = &S->ntrace;
+      sa.st_err = &S->err;
+      sa.out_buf = reinterpret_cast<int*>(ws + L.outbuf);
+      sa.trace_iter = trace_iter; sa.trace_err = trace_err; sa.cap = cap;
+      S_CUDA(cudaMemsetAsync(ws + L.bar, 0, 16, st));
+      S_CUDA(cudaMemsetAsync(ws + L.outbuf, 0, 16, st));
+      k_std_init<<<64, 256, 0, st>>>(sa.u0, n, sa.v0, m, S);
+      static bool attr = false;
+      if (!attr) {
+        S_CUDA(cudaFuncSetAttribute(k_std_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(StdFused::kSmemBytes)));
+        attr = true;
+      }
+      void* args[] = {&sa};
+      S_CUDA(cudaLaunchCooperativeKernel((const void*)k_std_fused, dim3(G), dim3(512), args, StdFused::kSmemBytes, st));
+      k_std_pick<<<64, 256, 0, st>>>(sa.u0, sa.u1, n, sa.v0, sa.v1, m, sa.out_buf, u, v);
+      if (flags & LSK_FLAG_COST) {
+        k_cost_rows<T><<<rblocks, 256, 0, st>>>(C, ldc, Km, L.ldk, n, m, u, v, term, S);
+        k_blocksum<T><<<nb, 256, 0, st>>>(term, n, blk, nullptr);
+        k_cost_finish<T><<<1, 1, 0, st>>>(n, blk, S);
+      }
+      k_results<T><<<1, 1, 0, st>>>(S, result, result_f, (flags & LSK_FLAG_COST) ? 1 : 0);
+      S_CUDA(cudaGetLastError());
+      return LSK_OK;
+    }
+  }
   auto check = [&](int kk, bool final) -> int32_t {
     k_nonfinite<T><<<8, 256, 0, st>>>(u, n, bad, act);
     k_nonfinite<T><<<8, 256, 0, st>>>(v, m, bad, act);

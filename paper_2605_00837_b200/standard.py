@@ -4,7 +4,9 @@
 the reference's deliberately unguarded twin of the log-domain solve
 (``solver.py:340-431``): K = exp(-C / eps) materialised once, then
 ``u = mu / (K v)``, ``v = nu / (K^T u)`` from u = v = 1, with the same
-checkpoint logic, trace, final extra check and cost. Overflow, underflow and
+checkpoint logic, trace, final extra check and cost (fp32 with m <= 8192: one
+persistent kernel reading K once per iteration, ``csrc/lsk_stdfused.cuh``).
+Overflow, underflow and
 division by zero propagate and surface as numerical_failure at the next
 checkpoint, as in the reference. One C-ABI call (``lsk_solve_standard_f32`` /
 ``_f64``, ``csrc/lsk_standard.cu``) per solve; precision follows
@@ -23,8 +25,11 @@ from .types import _STATUS_BY_CODE, STATUS_NUMERICAL_FAILURE, SolveReport
 __all__ = ["solve_standard_domain"]
 
 
-def solve_standard_domain(cost, mu, nu, config):
-    """(SolveReport, u, v) of the standard-domain iteration (see module doc)."""
+def solve_standard_domain(cost, mu, nu, config, *, fused=True):
+    """(SolveReport, u, v) of the standard-domain iteration (see module doc).
+
+    fp32 problems with m <= 8192 run the one-pass persistent kernel (one read of
+    K per iteration); ``fused=False`` forces the two-pass multi-kernel loop."""
     _check_dims(cost, mu, nu)
     torch = _torch()
     t0 = time.perf_counter()
@@ -53,7 +58,8 @@ def solve_standard_domain(cost, mu, nu, config):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     _lib.call("lsk_solve_standard_f64" if double else "lsk_solve_standard_f32", _ptr(Cp), ldc, n, m, _ptr(w_mu),
-              _ptr(w_nu), float(config.epsilon), float(config.tolerance), K, c, _lib.LSK_FLAG_COST, _ptr(u), _ptr(v),
+              _ptr(w_nu), float(config.epsilon), float(config.tolerance), K, c,
+              _lib.LSK_FLAG_COST | (0 if fused else _lib.LSK_FLAG_STD_MULTIKERNEL), _ptr(u), _ptr(v),
               _ptr(ti), _ptr(te), _ptr(res), _ptr(resf), _ptr(ws), wsb, _stream_ptr(torch))
     ev1.record()
     r, rf = res.cpu().numpy(), resf.cpu().numpy()

@@ -58,3 +58,27 @@ def test_standard_domain_dense_c2_shape(cuda_ok):
     rep2, _ = lsk.solve(C, w, w, cfg)
     assert rep.status == "converged" and rep2.status == "converged"
     assert abs(rep.transport_cost - rep2.transport_cost) <= 1e-4 * abs(rep2.transport_cost)
+
+
+@pytest.mark.parametrize("n,m,eps,K", [(2048, 2048, 0.02, 300), (1000, 777, 0.05, 200), (3000, 8192, 0.01, 120),
+                                       (48, 48, 2e-4, 100)])
+def test_fused_one_pass_vs_two_pass(cuda_ok, n, m, eps, K):
+    """The one-pass persistent standard-domain kernel against the two-pass multi-kernel
+    loop: same status, iterations and trace checkpoints, values to fp32 rounding
+    (including the small-eps failure, where both stop at the same checkpoint)."""
+    rng = np.random.default_rng(n + m)
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, nu = lsk.make_distribution(rng.uniform(0.5, 1.5, n)), lsk.make_distribution(rng.uniform(0.5, 1.5, m))
+    cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-7, max_iterations=K, check_interval=7)
+    r1, u1, v1 = lsk.solve_standard_domain(C, mu, nu, cfg)
+    r0, u0, v0 = lsk.solve_standard_domain(C, mu, nu, cfg, fused=False)
+    assert r1.status == r0.status and r1.iterations == r0.iterations
+    assert [k for k, _ in r1.error_trace] == [k for k, _ in r0.error_trace]
+    if r0.status == "numerical_failure":
+        assert np.isnan(r1.transport_cost)
+        return
+    np.testing.assert_allclose([e for _, e in r1.error_trace], [e for _, e in r0.error_trace], rtol=2e-2, atol=1e-8)
+    np.testing.assert_allclose(u1, u0, rtol=2e-4)
+    np.testing.assert_allclose(v1, v0, rtol=2e-4)
+    assert abs(r1.transport_cost - r0.transport_cost) <= 1e-5 * abs(r0.transport_cost)
