@@ -8,7 +8,6 @@ import os
 import re
 import subprocess
 
-import pytest
 
 from conftest import ROOT
 from paper_2605_00837_b200 import _lib

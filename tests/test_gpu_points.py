@@ -12,7 +12,7 @@ import pytest
 
 import lsk_oracle as O
 import paper_2605_00837_b200 as lsk
-from conftest import rel_max
+
 from inputs import fixture_points
 from paper_2605_00837_b200 import points as PT
 
