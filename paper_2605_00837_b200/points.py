@@ -76,6 +76,25 @@ class _PointsRun:
     __slots__ = ("B", "n", "m", "f", "g", "ti", "te", "res", "resf", "ev0", "ev1", "t0", "keep")
 
 
+# The expansion form c = |x|^2 + |y|^2 - 2 x.y (kernels translate every problem by
+# its first source point x0) carries an absolute rounding error of about
+# (|x - x0|^2 + |y - x0|^2) 2^-24 in c, i.e. that over eps (and the cost
+# normaliser) in every exponent. It is requested only when that bound stays
+# below 5e-5 -- the C5 RGB unit-cube problems at eps = 1e-2 sit at 3.6e-5 and are
+# parity-tested; wider clouds or smaller eps use the direct (x - y)^2 form.
+_EXPANSION_BOUND = 5e-5
+
+
+def _expansion_ok(Xb, Yb, eps, normalize):
+    x0 = Xb[:, :1, :]
+    rx = ((Xb - x0) ** 2).sum(axis=2).max(axis=1)
+    ry = ((Yb - x0) ** 2).sum(axis=2).max(axis=1)
+    # C.max() >= max_j |y_j - x0|^2 (x0 is a source point): a lower bound of the normaliser
+    div = np.where((normalize == "max") & (ry > 0), ry, 1.0)
+    bound = (rx + ry) * 2.0 ** -24 / (float(eps) * div)
+    return bool(np.all(bound <= _EXPANSION_BOUND))
+
+
 def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=False):
     torch = _torch()
     if config.precision != "single":
@@ -114,6 +133,8 @@ def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=F
     r.res = torch.zeros((B, 8), dtype=torch.int32, device="cuda")
     r.resf = torch.zeros((B, 2), dtype=torch.float32, device="cuda")
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
+    if expansion and not _expansion_ok(Xb, Yb, config.epsilon, normalize):
+        expansion = False
     flags |= _lib.LSK_FLAG_EXPANSION if expansion else 0
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
@@ -152,8 +173,9 @@ def solve_points_otf(X, Y, mu, nu, config, normalize="none", *, stale_shift=True
                      expansion=True):
     """One on-the-fly solve of points X (n, d) vs Y (m, d); see module doc.
     ``expansion`` (default on) evaluates the cost as |x|^2+|y|^2-2x.y in the
-    stale sweeps when eps >= 5e-3 (3 instead of 6 FP32 ops per pair; parity
-    tested at eps = 1e-2); below 5e-3 the direct form is always used."""
+    stale sweeps when eps >= 5e-3 and the rounding bound of that form is small
+    against eps (``_expansion_ok``; 3 instead of 6 FP32 ops per pair, parity
+    tested on the C5 shape); otherwise the direct form is used."""
     r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, comm, expansion)
     return _reports(r, return_device)[0]
 

@@ -1,0 +1,60 @@
+"""Randomised parity sweep of the on-the-fly points solver (C4/C5 kernels)
+against the oracle on the materialised fp64 cost: random sizes, dimension 1-3,
+weights, eps (both sides of the expansion-form gate), max-normalisation, check
+interval and cap; fixed iteration counts.
+
+Domain: the on-the-fly cost is formed in fp32 from coordinates translated by
+the first source point, so its absolute error is ~2^-23 R |x - y| (R the cloud
+radius) where the reference's fp32(C64) has 2^-24 |x - y|^2; with eps the
+exponent error grows like R / sqrt(eps) for the pairs that carry the mass.
+Unit-scale clouds (the C4/C5 configs) or max-normalised costs keep it far
+below the parity tolerance; large unnormalised clouds at eps < 5e-3 are the
+dense path's job (fp64-exact cost build), DESIGN.md."""
+
+import numpy as np
+import pytest
+
+import lsk_oracle as O
+import paper_2605_00837_b200 as lsk
+from paper_2605_00837_b200 import points as PT
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(seed):
+    rng = np.random.default_rng(5000 + seed)
+    n, m, d = int(rng.integers(1, 900)), int(rng.integers(1, 2500)), int(rng.integers(1, 4))
+    normalize = "max" if rng.random() < 0.5 else "none"
+    eps = float(rng.choice([1e-3, 3e-3, 5e-3, 1e-2, 5e-2]))
+    # radius: wide clouds only where the cost is normalised or eps is not small
+    wide = normalize == "max" or eps >= 1e-2
+    s = rng.uniform(0.3, 3.0) if wide else rng.uniform(0.3, 1.0)
+    X = rng.uniform(-1, 1, (n, d)) * s
+    Y = rng.uniform(-1, 1, (m, d)) * s + rng.uniform(-0.5, 0.5, d) * min(s, 1.0)
+    wa = np.ones(n) if rng.random() < 0.5 else rng.uniform(0.2, 2.0, n)
+    wb = np.ones(m) if rng.random() < 0.5 else rng.uniform(0.2, 2.0, m)
+    return X, Y, wa, wb, normalize, eps, int(rng.integers(2, 40)), int(rng.integers(1, 12))
+
+
+@pytest.mark.parametrize("seed", list(range(40)))
+def test_random_points_vs_oracle(cuda_ok, seed):
+    X, Y, wa, wb, normalize, eps, K, c = problem(seed)
+    mu, nu = lsk.make_distribution(wa), lsk.make_distribution(wb)
+    cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K, check_interval=c)
+    rep, pot = PT.solve_points_otf(X, Y, mu, nu, cfg, normalize=normalize)
+    C64 = O.sq_euclidean_cost(X, Y)
+    if normalize == "max":
+        C64 = O.max_normalized(C64)
+    with np.errstate(all="ignore"):
+        ref = O.solve(C64, mu.weights, nu.weights, eps, tol=1e-30, max_iter=K, check=c)
+    assert rep.status == ref["status"] and rep.iterations == ref["iterations"], (seed, rep.status, ref["status"])
+    if ref["status"] == "numerical_failure":
+        return
+    scale = max(np.abs(ref["alpha"]).max(), np.abs(ref["beta"]).max())
+    ea = np.abs(np.asarray(pot.alpha) - ref["alpha"]).max() / scale
+    eb = np.abs(np.asarray(pot.beta) - ref["beta"]).max() / scale
+    assert ea <= 1e-5 and eb <= 1e-5, (seed, X.shape, Y.shape, normalize, eps, K, ea, eb)
+    # the cost sums C_ij P_ij with C_ij formed on the fly in fp32 (relative error up to
+    # ~2^-23 R / |x - y| on the near pairs that carry the mass): 5e-5 here, 1e-5 for
+    # the potentials
+    assert abs(rep.transport_cost - ref["cost"]) <= 5e-5 * abs(ref["cost"]) + 1e-7
