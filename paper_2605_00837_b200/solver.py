@@ -254,17 +254,14 @@ def update_beta(cost, mu, alpha, eps, plan=ReductionPlan(), transposed_cost=None
     """
     torch = _half_inputs(cost, eps)
     if transposed_cost is not None:
-        shp = tuple(np.shape(transposed_cost)) if not hasattr(transposed_cost, "shape") else tuple(transposed_cost.shape)
+        tv = getattr(transposed_cost, "values", transposed_cost)  # an array (reference) or a CostMatrix
+        shp = tuple(tv.shape) if hasattr(tv, "shape") else tuple(np.shape(tv))
         rows, cols = (cost.rows, cost.cols)
         if shp != (cols, rows):
             raise DimensionMismatch(f"transposed_cost has shape {shp}, expected {(cols, rows)}")
     if _is_f64(alpha):
         return _s64.update_beta(cost, mu, alpha, eps)
     C = to_device_cost(cost)
-    if transposed_cost is not None:
-        shp = tuple(np.shape(transposed_cost)) if not hasattr(transposed_cost, "shape") else tuple(transposed_cost.shape)
-        if shp != (C.cols, C.rows):
-            raise DimensionMismatch(f"transposed_cost has shape {shp}, expected {(C.cols, C.rows)}")
     a, lmu = _vecs(torch, alpha, mu.log_weights)
     out = torch.empty(C.cols, dtype=torch.float32, device="cuda")
     wsb = _lib.load().lsk_update_beta_workspace_bytes(C.rows, C.cols)
