@@ -385,7 +385,7 @@ int32_t lsk_update_alpha_f32(const float* C, int64_t ldc, int32_t n, int32_t m, 
 
 static int beta_rowsplit(int n, int m) {
   int tiles = (m + 1023) / 1024;
-  int want = (2 * num_sms() + tiles - 1) / tiles;  // ~2 CTAs per SM
+  int want = (8 * num_sms() + tiles - 1) / tiles;  // ~8 CTAs per SM: rows in flight for HBM
   int rs = (n + want - 1) / want;
   if (rs < 64) rs = 64;
   return rs;

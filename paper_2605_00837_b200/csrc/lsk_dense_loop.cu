@@ -34,7 +34,7 @@ inline size_t al(size_t x) { return (x + 255) / 256 * 256; }
 
 int beta_parts(int n, int m, int sms, int* rs_out) {
   const int tiles = (m + 1023) / 1024;
-  const int want = (2 * sms + tiles - 1) / tiles;
+  const int want = (8 * sms + tiles - 1) / tiles;  // ~8 CTAs per SM: enough rows in flight for HBM
   int rs = (n + want - 1) / want;
   if (rs < 64) rs = 64;
   *rs_out = rs;
