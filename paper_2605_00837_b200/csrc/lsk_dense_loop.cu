@@ -138,8 +138,12 @@ int32_t solve_dense_loop(const float* C, int64_t ldc, int32_t n, int32_t m, cons
   int32_t rc;
   for (int k = 1; k <= K; ++k) {
     if (k > 1 && (k - 1) % c == 0 && (rc = check(k - 1, false))) return rc;
-    lsk::k_row_lse<lsk::kRowAlpha><<<n, 256, 0, st>>>(C, ldc, n, m, nullptr, G[(k - 1) & 1], log_nu, nullptr,
-                                                      nullptr, inv_eps, neg_eps, F[k & 1], act);
+    if (k > 1)  // one read of the row, shifted by the stale f (exact fallback per row)
+      lsk::k_row_alpha_stale<<<n, 256, 0, st>>>(C, ldc, n, m, F[(k - 1) & 1], G[(k - 1) & 1], log_nu, inv_eps, neg_eps,
+                                                F[k & 1], act);
+    else
+      lsk::k_row_lse<lsk::kRowAlpha><<<n, 256, 0, st>>>(C, ldc, n, m, nullptr, G[(k - 1) & 1], log_nu, nullptr,
+                                                        nullptr, inv_eps, neg_eps, F[k & 1], act);
     lsk::k_col_pairs<<<dim3((m + 1023) / 1024, parts), 256, 0, st>>>(C, ldc, n, m, F[k & 1], log_mu, inv_eps, rs,
                                                                     pairs, act);
     lsk::k_col_combine<<<(m + 255) / 256, 256, 0, st>>>(pairs, parts, m, neg_eps, G[k & 1], act);

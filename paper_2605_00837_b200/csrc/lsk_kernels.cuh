@@ -61,6 +61,47 @@ static __global__ void __launch_bounds__(256) k_row_lse(const float* __restrict_
   }
 }
 
+// One-pass alpha row LSE for the m > 8192 loop: shifted by the stale row shift
+// -f_i^{k-1} * inv_eps (as the fused solver); a row whose shifted
+// sum leaves [1e-20, 1e30] (or whose previous f is not finite) redoes the exact
+// two-pass LSE from L1/L2. One read of the row instead of two sweeps.
+static __global__ void __launch_bounds__(256) k_row_alpha_stale(const float* __restrict__ C, long long ldc, int n,
+                                                               int m, const float* __restrict__ fprev,
+                                                               const float* __restrict__ other,
+                                                               const float* __restrict__ lw, float inv_eps,
+                                                               float neg_eps, float* __restrict__ out,
+                                                               const int* __restrict__ active = nullptr) {
+  __shared__ float red[64];
+  if (active && !*active) return;
+  const int i = blockIdx.x;
+  const float* Ci = C + (long long)i * ldc;
+  const float fo = fprev[i];
+  float M = __fmul_rn(-fo, inv_eps);
+  float s[1] = {0.f};
+  if (isfinite(M)) {
+    const float sl = __fmul_rn(M, kLog2e);
+    for (int j = threadIdx.x; j < m; j += 256) s[0] += exp_shifted(arg3(other[j], Ci[j], inv_eps, lw[j]), sl);
+    block_reduce<256, 1, false>(s, red);
+  }
+  __shared__ int redo;
+  if (threadIdx.x == 0) redo = !(isfinite(M) && s[0] >= 1e-20f && s[0] <= 1e30f);
+  __syncthreads();
+  if (redo) {  // exact two-pass (reduction.py:179-208)
+    float mx[1] = {-INFINITY};
+    for (int j = threadIdx.x; j < m; j += 256) mx[0] = fmax_nan(mx[0], arg3(other[j], Ci[j], inv_eps, lw[j]));
+    __syncthreads();
+    block_reduce<256, 1, true>(mx, red);
+    M = mx[0];
+    const float Ms = (fabsf(M) <= 3.402823466e38f) ? M : 0.f;
+    const float sl = __fmul_rn(Ms, kLog2e);
+    s[0] = 0.f;
+    for (int j = threadIdx.x; j < m; j += 256) s[0] += exp_shifted(arg3(other[j], Ci[j], inv_eps, lw[j]), sl);
+    __syncthreads();
+    block_reduce<256, 1, false>(s, red + 32);
+  }
+  if (threadIdx.x == 0) out[i] = __fmul_rn(neg_eps, lse_finish(M, s[0]));
+}
+
 // Column LSE of the beta argument y_ij = arg3(alpha_i, C_ij, inv, log_mu_i):
 // CTA (bx, by) owns columns [bx*1024, +1024) (256 threads x float4, coalesced
 // 4 KB row segments) and rows [by*rs, +rs); each thread keeps a chunked online

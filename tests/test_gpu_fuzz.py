@@ -52,3 +52,27 @@ def test_random_problem_vs_oracle(cuda_ok, seed):
     assert ea <= 1e-5 and eb <= 1e-5, (seed, n, m, eps, K, ea, eb)
     assert abs(rep.transport_cost - ref["cost"]) <= 1e-5 * abs(ref["cost"]) + 1e-7
     assert [k for k, _ in rep.error_trace] == [k for k, _ in ref["trace"]]
+
+
+@pytest.mark.parametrize("seed", list(range(6)))
+def test_wide_m_loop_vs_oracle(cuda_ok, seed):
+    """m > 8192 runs the multi-kernel loop (one-pass stale row LSE with exact fallback,
+    column (max, sumexp) partials, device-side checks): same bar against the oracle."""
+    rng = np.random.default_rng(3000 + seed)
+    n, m = int(rng.integers(1, 80)), int(rng.integers(8193, 13000))
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C64 = ((X[:, None, :] - Y[None, :, :]) ** 2).sum(axis=2)
+    wa = np.ones(n) if seed % 2 else rng.uniform(0.2, 2.0, n)
+    wb = np.ones(m) if seed % 3 else rng.uniform(0.2, 2.0, m)
+    eps = float(rng.choice([1e-3, 1e-2, 5e-2]))
+    K, c = int(rng.integers(2, 30)), int(rng.integers(1, 8))
+    mu, nu = lsk.make_distribution(wa), lsk.make_distribution(wb)
+    cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K, check_interval=c)
+    rep, pot = lsk.solve(lsk.make_cost_matrix(n, m, C64), mu, nu, cfg)
+    with np.errstate(all="ignore"):
+        ref = O.solve(C64, mu.weights, nu.weights, eps, tol=1e-30, max_iter=K, check=c)
+    assert rep.status == ref["status"] and rep.iterations == ref["iterations"]
+    scale = max(np.abs(ref["alpha"]).max(), np.abs(ref["beta"]).max())
+    assert np.abs(pot.alpha - ref["alpha"]).max() <= 1e-5 * scale
+    assert np.abs(pot.beta - ref["beta"]).max() <= 1e-5 * scale
+    assert abs(rep.transport_cost - ref["cost"]) <= 1e-5 * abs(ref["cost"]) + 1e-7
