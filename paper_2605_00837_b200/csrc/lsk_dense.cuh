@@ -431,6 +431,11 @@ struct DenseSolver {
       mbar_arrive(&bsum[step & 1]);
     }
   }
+  // block-barrier hand-off of the multiplicative pass: the warp sum goes to red
+  // and the next step's __syncthreads publishes it (no mbarrier)
+  __device__ __forceinline__ void post_bar(unsigned step, float s) {
+    if ((threadIdx.x & 31) == 0) red[kRedRows + (step & 1) * NW + (threadIdx.x >> 5)] = s;
+  }
   __device__ __forceinline__ void wait_posted(unsigned step) {
 #ifndef LSK_X_NOWAIT
     mbar_wait(&bsum[step & 1], (step >> 1) & 1);
@@ -638,7 +643,7 @@ struct DenseSolver {
     float s;
     f_part_e(row, fold_cur, s, eA);
     s = warp_sum(s);
-    post(g0, s, 0.f, false);
+    post_bar(g0, s);
     const float* row_prev = row;
     int st_prev = st_cur, st_pp = 0;
     int i_prev = i_cur;
@@ -654,7 +659,7 @@ struct DenseSolver {
       row = wait_head();
       probe_head();
       const unsigned sp = g0 + q - 1;
-      wait_posted(sp);
+      __syncthreads();  // every warp's sum of row q-1 is in red (and row q-2 is done)
       if (q >= 2) refill(st_pp, P, q - 2);
       const float S = sum_warps(kRedRows + (sp & 1) * NW);
       f_part_e(row, fold_cur, s, eout);
@@ -663,7 +668,7 @@ struct DenseSolver {
       col_update<true>(row_prev, f_prev, fold_prev, lmu_prev, ein, s);
       carry_f1 = f_prev;
       carry_l1 = lmu_prev;
-      post(g0 + q, s, 0.f, false);
+      post_bar(g0 + q, s);
       st_pp = st_prev;
       row_prev = row;
       st_prev = st_cur;
@@ -679,7 +684,7 @@ struct DenseSolver {
     const bool odd = q < rows;
     if (odd) step(q, eA, eB);
     const unsigned sl = g0 + rows - 1;
-    wait_posted(sl);
+    __syncthreads();
     if (rows >= 2) refill(st_pp, P, rows - 2);
     const float f_last = finish_f(row_prev, fold_prev, sum_warps(kRedRows + (sl & 1) * NW));
     if (threadIdx.x == 0) fnew[i_prev] = f_last;
@@ -687,7 +692,7 @@ struct DenseSolver {
     else col_update<false>(row_prev, f_last, fold_prev, lmu_prev, eA, s);
     __syncthreads();
     refill(st_prev, P, rows - 1);
-    gstep = g0 + rows;
+    // gstep (the SUMS mbarrier phase count) is untouched: this pass hands off through __syncthreads
     carry_f0 = f_last;
     carry_l0 = lmu_prev;
     carry_pass = rows > 1 ? P + 1 : -1;
