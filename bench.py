@@ -401,13 +401,15 @@ def main():
                        "guard_stats_last_step": guard},
             "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": 3 * args.steps}
-    if rank == 0 and not args.no_extra:
+    # single-GPU extras (the other configs' rates, the CPU baseline) at N = 1 only
+    if rank == 0 and ws == 1 and not args.no_extra:
         line["other_configs"] = other_configs()
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(X, Y, iters=int(os.environ.get("LSK_CPU_ITERS", "80")))
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
+        barrier()
         dist.destroy_process_group()
 
 
