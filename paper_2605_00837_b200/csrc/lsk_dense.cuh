@@ -22,11 +22,16 @@
 //    known -- adds exp(y_ij - s_j) into its per-column accumulators, where
 //    y_ij = fl(fl(fl(f_i^k - C_ij) * inv_eps) + log mu_i) is the reference's
 //    beta argument and s_j = fl(-g_j^{k-1} * inv_eps) the stale column shift
-//    (terms are bounded by mu_i / nu_j, no overflow). The row LSE
-//    of row q and the column update of row q-1 share one __syncthreads.
+//    (terms are bounded by mu_i / nu_j, no overflow). Warps hand
+//    the row sums to each other through an mbarrier per step (no block
+//    barrier); thread 0 refills a ring stage once every warp is two rows past it.
 //    A grid-wide fixed-order combine of the G per-CTA column partials forms
 //    g^k. Sums outside [1e-20, 1e30] fall back to the exact max shift (rows:
 //    from the smem copy of the row; columns: an exact (max, sumexp) pass).
+//  * Uniform targets, eps >= 1e-3, n m >= 2^20 (fused_pass_mult): the g-side
+//    term of (i, j) is the f-side term times 2^(a_i + b) in exact arithmetic,
+//    so the column update is one FFMA2 per pair from the f-side terms kept in
+//    registers (no second cost read, no second ex2); a block barrier per row.
 //  * Every c iterations the pass of k+1 also evaluates the reference marginal
 //    error formula for iterate k (solver.py:97-104) from the same on-chip row
 //    -- no extra HBM pass, no host sync; f/g are double buffered so a stop at
