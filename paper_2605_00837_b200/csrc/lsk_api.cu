@@ -51,16 +51,16 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // ---- persistent dense solver instances: (NT, V, R, STAGES) by row capacity W
 using Solver1k = lsk::DenseSolver<256, 1, 16>;
-using Solver2k = lsk::DenseSolver<512, 1, 16>;
-using Solver4k = lsk::DenseSolver<512, 2, 12>;
-using Solver8k = lsk::DenseSolver<512, 4, 6>;
+using Solver2k = lsk::DenseSolver<256, 2, 16>;
+using Solver4k = lsk::DenseSolver<256, 4, 12>;
+using Solver8k = lsk::DenseSolver<256, 8, 6>;
 // uniform target weights (LSK_FLAG_UNIFORM_NU); the 8k one runs 8 warps x 32
 // columns (255 registers): with the multiplicative column update the per-row
 // bookkeeping, not the MUFU, bounds the step, and 32 columns per thread halve it
 // per column (10.3 vs 11.7 ms per 200 C2 iterations)
 using Solver1kU = lsk::DenseSolver<256, 1, 16, true>;
-using Solver2kU = lsk::DenseSolver<512, 1, 16, true>;
-using Solver4kU = lsk::DenseSolver<512, 2, 12, true>;
+using Solver2kU = lsk::DenseSolver<256, 2, 16, true>;
+using Solver4kU = lsk::DenseSolver<256, 4, 12, true>;
 using Solver8kU = lsk::DenseSolver<256, 8, 6, true>;
 
 template <class SV>
