@@ -303,7 +303,7 @@ struct StdLayout {
   size_t u0, u1, v0, v1, fpart, errp, flagp, bar, outbuf;
   long long ldk;
 };
-using StdFused = lsk::StdSolver<512, 4, 6>;
+using StdFused = lsk::StdSolver<256, 8, 6>;
 constexpr int kStdW = StdFused::W;
 template <class T>
 StdLayout std_layout(int n, int m) {
@@ -415,7 +415,7 @@ int32_t solve_standard(const T* C, int64_t ldc, int32_t n, int32_t m, const T* m
         attr = true;
       }
       void* args[] = {&sa};
-      S_CUDA(cudaLaunchCooperativeKernel((const void*)k_std_fused, dim3(G), dim3(512), args, StdFused::kSmemBytes, st));
+      S_CUDA(cudaLaunchCooperativeKernel((const void*)k_std_fused, dim3(G), dim3(StdFused::NW * 32), args, StdFused::kSmemBytes, st));
       k_std_pick<<<64, 256, 0, st>>>(sa.u0, sa.u1, n, sa.v0, sa.v1, m, sa.out_buf, u, v);
       if (flags & LSK_FLAG_COST) {
         k_cost_rows<T><<<rblocks, 256, 0, st>>>(C, ldc, Km, L.ldk, n, m, u, v, term, S);
