@@ -244,20 +244,21 @@ struct DenseSolver {
       const float L = __ldg(a.log_nu);
       lnu2 = pk2(L, L);
       bcol = -__fmul_rn(L, kLog2e);
-      return;
-    }
+    } else {
 #pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float t[4];
+      for (int v = 0; v < V; ++v) {
+        float t[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = col(v, q);
-        t[q] = j < a.m ? __ldg(a.log_nu + j) : -INFINITY;
+        for (int q = 0; q < 4; ++q) {
+          const int j = col(v, q);
+          t[q] = j < a.m ? __ldg(a.log_nu + j) : -INFINITY;
+        }
+        ln2[2 * v] = pk2(t[0], t[1]);
+        ln2[2 * v + 1] = pk2(t[2], t[3]);
       }
-      ln2[2 * v] = pk2(t[0], t[1]);
-      ln2[2 * v + 1] = pk2(t[2], t[3]);
     }
   }
+
   // g^{k-1} into registers (+ the stale column shifts); returns "some owned g is non-finite"
   __device__ bool load_columns(const float* g) {
     bool bad = false;

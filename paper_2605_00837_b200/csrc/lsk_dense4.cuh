@@ -329,7 +329,7 @@ struct DenseV4 {
   template <int MODE, bool CHECK>
   __device__ unsigned pass(const float* fprev, float* fnew) {
     const unsigned P = npass++;
-    const bool with_f = MODE != 4, with_g = MODE <= 1 || MODE == 4;
+    const bool with_f = MODE != 4;
     const bool interleave = MODE <= 1;
     const unsigned target = (gpasses + 1) * unsigned(SR);
     const int total = interleave ? S * SR + S * T : (with_f ? S * SR : S * T);
