@@ -1,3 +1,4 @@
+"""fp64 (precision="double") dense solve timing at n=m=2048 and 8192: python tools/profile_f64.py"""
 import sys, numpy as np
 sys.path.insert(0, '.')
 import paper_2605_00837_b200 as lsk
