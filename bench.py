@@ -11,16 +11,25 @@ iterations and the transport cost included), i.e. the whole hot path.
            no flush is needed between steps; the solver itself alternates
            the sweep direction and reuses L2 within a step)
   e2e      the same metric through the public drop-in API with HOST buffers:
-           CostMatrix(fp64, pinned) in, potentials out, H2D/D2H inside the
-           timed region
+           the reference's own input type, CostMatrix(numpy fp64, pageable),
+           in; numpy potentials out; H2D/D2H inside the timed region
   roofline the persistent solver kernel vs measured HBM bandwidth
   cpu_baseline  the oracle port of the reference (bit-exact numpy restatement,
-           all host threads) on a bounded sample
+           all host threads) on bounded samples of every config
+
+Multi-GPU (torchrun, one rank per GPU): the sharded configs.
+Every line carries ``scaling_configs``:
+  C4  one rigid-pair problem n=m=65536 (generate_rigid_pair, C/C.max(),
+      eps=1e-3, on the fly) sharded over the N ranks -- strong scaling,
+      column-partials design (and owner computes for comparison)
+  C5  256 RGB problems n=m=4096, eps=1e-2, 200 iterations, 256/N per rank,
+      no communication -- weak scaling of the batch split
+At N = 1 the headline is C2 (BENCH); at N > 1 the headline ``value`` is the
+C4 sharded iterations/s (the north star's scaling target) -- C2 is a
+single-GPU config and is never replicated to fake scaling.
 
 ``--impl reference`` times only the reference CPU path (the oracle port, the
-reference's numpy algorithm) on the same config. Multi-GPU (torchrun): each
-rank solves its own C2 problem (independent problems split across GPUs, no
-communication) -- weak scaling; value = iterations of all ranks / max time.
+reference's numpy algorithm) on the C2 config.
 """
 
 import argparse
@@ -116,6 +125,17 @@ def problem(seed=0):
     return X, Y
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(X, Y, iters=8):
     """Oracle port (bit-exact restatement of the reference solve) on all host cores."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -130,9 +150,70 @@ def cpu_baseline(X, Y, iters=8):
     O.solve(C32, w, w, EPS, tol=1e-30, max_iter=iters, check=CHECK, CT=CT)
     dt = time.perf_counter() - t
     return {"value": iters / dt, "unit": "iters/s", "cores": O.host_threads(), "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{iters} iterations of C2 (n=m=8192, eps=1e-3) + final check + transport cost, "
                       f"oracle/lsk_oracle.py (bit-exact numpy restatement of the reference), "
                       f"{O.host_threads()} threads, {dt:.1f} s"}
+
+
+def cpu_baselines_other():
+    """The reference algorithm (oracle port, all host threads) on bounded samples
+    of C1, C3, C4 and C5 (SURVEY 8(d) CPU baseline; reference timing
+    convention cli.py:236-241: the solve's own loop + cost)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import lsk_oracle as O
+
+    out = {"cpu_model": cpu_model(), "cores": O.host_threads(), "kind": "port"}
+    # C1 as-is: n=m=1024, eps=1e-2, 200 iterations
+    X, Y = O.uniform_points(1024, 2, 0)
+    C = O.sq_euclidean_cost(X, Y).astype(np.float32)
+    w = np.full(1024, 1.0 / 1024)
+    t = time.perf_counter()
+    O.solve(C, w, w, 1e-2, tol=1e-30, max_iter=200, check=10)
+    dt = time.perf_counter() - t
+    out["C1"] = {"value": 200 / dt, "unit": "iters/s", "sample": "the whole C1 solve as-is (200 iterations)",
+                 "seconds": dt}
+    # C3: eps=1e-4 at n=m=8192, fixed K=20
+    X, Y = O.uniform_points(N, 2, 0)
+    C = O.sq_euclidean_cost(X, Y).astype(np.float32)
+    CT = np.ascontiguousarray(C.T)
+    w = np.full(N, 1.0 / N)
+    t = time.perf_counter()
+    O.solve(C, w, w, 1e-4, tol=1e-30, max_iter=20, check=10, CT=CT)
+    dt = time.perf_counter() - t
+    out["C3"] = {"value": 20 / dt, "unit": "iters/s",
+                 "sample": "20 iterations of C3 (n=m=8192, eps=1e-4); the run to 1e-6 is not CPU-feasible "
+                           f"(~1e4+ iterations; {1e4 * dt / 20 / 3600:.1f} h extrapolated for 1e4)"}
+    del C, CT
+    # C5: 4 problems x 20 iterations of n=m=4096 RGB (eps=1e-2), scaled to 256 x 200
+    t = time.perf_counter()
+    for b in range(4):
+        Xb, Yb = O.uniform_points(4096, 3, b)
+        Cb = O.sq_euclidean_cost(Xb, Yb).astype(np.float32)
+        wb = np.full(4096, 1.0 / 4096)
+        O.solve(Cb, wb, wb, 1e-2, tol=1e-30, max_iter=20, check=10)
+    dt = time.perf_counter() - t
+    out["C5"] = {"value": 4 * 20 / dt, "unit": "problem-iters/s",
+                 "sample": "4 problems x 20 iterations (cost build included); EXTRAPOLATED to 256 x 200: "
+                           f"{256 * 200 * dt / 80 / 3600:.2f} h"}
+    # C4: one f half-step over a 1024-row slab of the 65536^2 rigid-pair cost (C/C.max()),
+    # extrapolated x64 rows x2 half-steps (the cost cannot be materialised as-is: SURVEY 8(c))
+    from paper_2605_00837_b200 import generate_rigid_pair
+
+    Xr, Yr, _ = generate_rigid_pair(65536, 3, 0.1, [0.1, 0.0, 0.0], 0.01, 0)
+    cmax = 3.0914804297769676  # SURVEY G4: exact max of the fp64 cost
+    t = time.perf_counter()
+    Cs = (O.sq_euclidean_cost(Xr[:1024], Yr) / cmax).astype(np.float32)
+    g = np.zeros(65536, np.float32)
+    lw = np.full(65536, np.float32(np.log(1.0 / 65536)), np.float32)
+    inv, neg = np.float32(1.0) / np.float32(1e-3), -np.float32(1e-3)
+    O.row_update(Cs, g, lw, inv, neg)
+    dt = time.perf_counter() - t
+    per_iter = dt * 64 * 2
+    out["C4"] = {"value": 1.0 / per_iter, "unit": "iters/s",
+                 "sample": "EXTRAPOLATED: one f half-step over a 1024-row slab of C4 (cost block built in fp64 "
+                           f"and cast, as the reference) x 64 slabs x 2 half-steps = {per_iter:.1f} s/iteration"}
+    return out
 
 
 def other_configs():
@@ -148,7 +229,7 @@ def other_configs():
     sm, mhz = 148, 1965.0
     mufu_pairs = 16 * sm * mhz * 1e6  # one ex2 per pair evaluation
 
-    def dense(n, eps, K, seed=0, tol=1e-30, reps=2):
+    def dense(n, eps, K, seed=0, tol=1e-30, reps=2, mult=True):
         rng = np.random.Generator(np.random.PCG64(seed))
         X = rng.uniform(0.0, 1.0, (n, 2))
         Y = rng.uniform(0.0, 1.0, (n, 2))
@@ -158,7 +239,7 @@ def other_configs():
         cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=tol, max_iterations=K)
         ws = None
         for _ in range(reps):
-            r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, ws=ws, uniform_nu=True)
+            r, ws = S._launch_solve(torch, C, lm, lm, mu, cfg, ws=ws, uniform_nu=True, mult=mult)
         torch.cuda.synchronize()
         res = r.res.cpu().numpy()
         sec = r.ev0.elapsed_time(r.ev1) * 1e-3
@@ -179,6 +260,9 @@ def other_configs():
                 break
         return out
 
+    v, _ = dense(8192, 1e-3, 1000, mult=False)
+    out["C2_direct"] = {"workload": "C2 with the direct g-side arithmetic (LSK_FLAG_NO_MULT): every argument "
+                                    "rounded exactly as the reference", "iters_per_s": v}
     v, _ = dense(1024, 1e-2, 200)
     out["C1"] = {"workload": "dense n=m=1024 2-D points, eps=1e-2, 200 iterations", "iters_per_s": v,
                  "ms_per_solve": 200 / v * 1e3}
@@ -190,31 +274,6 @@ def other_configs():
     # the paper's headline shape (n=m=8192, eps=1e-2, solve to the default tolerance); the paper
     # reports 371.6 ms for 82 iterations on an RTX 3090 (its problem law is unstated)
     out["paper_shape_eps1e-2_to_tol"] = time_to_tol(8192, 1e-2, 10000, [1e-6])
-    # C4: rigid pair n=m=65536 3-D, C/C.max(), eps=1e-3, on the fly, 1 GPU
-    n, K = 65536, 20
-    rng = np.random.Generator(np.random.PCG64(0))
-    X = rng.uniform(0, 1, (n, 3))
-    Y = X + rng.normal(0, 0.01, X.shape) + np.array([0.1, 0.0, 0.0])
-    cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=K)
-    for _ in range(2):
-        rep, _ = PT.solve_points_otf(X, Y, None, None, cfg, normalize="max")
-    pairs = 2.0 * n * n * K / rep.device_seconds
-    out["C4"] = {"workload": "on-the-fly 3-D points n=m=65536, C/max, eps=1e-3, 20 iterations, 1 GPU",
-                 "iters_per_s": K / rep.device_seconds, "pair_evals_per_s": pairs,
-                 "roofline": {"bound": "mufu+fp32", "frac": pairs / mufu_pairs,
-                              "peak_pair_evals_per_s": mufu_pairs, "rule": "16 ex2/clk/SM x 148 SM x 1.965 GHz"}}
-    # C5: 32 RGB problems of 4096 (one GPU's share of 256 over 8), eps=1e-2, 200 iterations
-    B, K = 32, 200
-    Xs = np.stack([np.random.Generator(np.random.PCG64(b)).uniform(0, 1, (4096, 3)) for b in range(B)])
-    Ys = np.stack([np.random.Generator(np.random.PCG64(1000 + b)).uniform(0, 1, (4096, 3)) for b in range(B)])
-    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=K)
-    for _ in range(2):
-        outs = PT.solve_points_batched(Xs, Ys, cfg)
-    dev = outs[0][0].device_seconds
-    pairs = 2.0 * B * 4096 * 4096 * K / dev
-    out["C5"] = {"workload": "32 batched on-the-fly RGB problems n=m=4096, eps=1e-2, 200 iterations (1/8 of 256)",
-                 "problem_iters_per_s": B * K / dev, "ms_per_batch": dev * 1e3, "pair_evals_per_s": pairs,
-                 "roofline": {"bound": "mufu+fp32", "frac": pairs / mufu_pairs}}
     # SURVEY 8(f) consumers: standard-domain solve and the colour-transfer recolour
     n, K = 8192, 200
     rng = np.random.Generator(np.random.PCG64(0))
@@ -274,36 +333,15 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--iters", type=int, default=KITER)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the other-config rate lines")
-    ap.add_argument("--exact", action="store_true", help="exact two-pass variant instead of stale shift")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
-
+def c2_line(args, clocks_index):
+    """The C2 headline (single GPU): device-resident rate, e2e, roofline."""
     import torch
-    import torch.distributed as dist
 
     import paper_2605_00837_b200 as lsk
     from paper_2605_00837_b200 import solver as S
 
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if ws > 1:
-            dist.barrier()
-
-    X, Y = problem(rank)  # each rank its own independent problem (weak scaling)
+    local = clocks_index
+    X, Y = problem(0)
     K = args.iters
     cfg = lsk.SinkhornConfig(epsilon=EPS, tolerance=1e-30, max_iterations=K, check_interval=CHECK)
     C = lsk.squared_euclidean_cost(X, Y)  # fp32(C64) on the device
@@ -315,11 +353,10 @@ def main():
     wsbuf = None
     for _ in range(args.warmup):
         r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf,
-                                       uniform_nu=True)
+                                   uniform_nu=True, mult=not args.direct)
     torch.cuda.synchronize()
     res = r.res.cpu().numpy()
     assert int(res[1]) == K, res
-    barrier()
     torch.cuda.synchronize()
     evs = []
     with Clocks(local) as clk:
@@ -328,44 +365,34 @@ def main():
         e0.record()
         for _ in range(args.steps):
             r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf,
-                                       uniform_nu=True)
+                                       uniform_nu=True, mult=not args.direct)
             evs.append((r.ev0, r.ev1))
         e1.record()
         torch.cuda.synchronize()
-    barrier()
     t_total = e0.elapsed_time(e1) * 1e-3
     kern = [a.elapsed_time(b) * 1e-3 for a, b in evs]  # solver launch alone (the dominant kernel)
-    if ws > 1:
-        t = torch.tensor([t_total], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_total = float(t.item())
-    value = ws * K * args.steps / t_total
+    value = K * args.steps / t_total
     guard = r.res.cpu().numpy()[4:6].tolist()
 
-    # ---- e2e through the public API with host (pinned fp64) buffers
-    C64 = torch.empty((N, N), dtype=torch.float64, pin_memory=True)
+    # ---- e2e through the public API with the reference's own input type: a
+    # CostMatrix holding a numpy fp64 (n, m) array (pageable host memory)
     Xd = torch.from_numpy(X).to("cuda")
     Yd = torch.from_numpy(Y).to("cuda")
-    C64.copy_(((Xd[:, None, :] - Yd[None, :, :]) ** 2).sum(-1).cpu())  # input prep, untimed
+    C64 = ((Xd[:, None, :] - Yd[None, :, :]) ** 2).sum(-1).cpu().numpy()  # input prep, untimed
     del Xd, Yd
-    host_cost = lsk.CostMatrix(values=C64, value_range=1.0)
-    e2e_steps = max(2, min(args.steps, 3))
-    for _ in range(1):
-        lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact)
-    barrier()
+    host_cost = lsk.CostMatrix(values=C64)
+    e2e_steps = max(3, args.steps)
+    lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=not args.direct)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        rep, pot = lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact)
+        rep, pot = lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=not args.direct)
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_e2e = float(t.item())
-    e2e = {"value": ws * K * e2e_steps / t_e2e, "unit": "iters/s", "h2d_bytes_per_step": N * N * 8 + 3 * N * 4,
+    e2e = {"value": K * e2e_steps / t_e2e, "unit": "iters/s", "h2d_bytes_per_step": N * N * 8 + 3 * N * 4,
            "d2h_bytes_per_step": 2 * N * 4 + 8 * 4 + 2 * 4 + (K // CHECK + 1) * 8,
-           "path": "paper_2605_00837_b200.solve(CostMatrix(pinned fp64 host), ...) -> numpy potentials"}
+           "path": "paper_2605_00837_b200.solve(CostMatrix(numpy fp64, pageable host), ...) -> numpy potentials",
+           "steps": e2e_steps}
 
     # ---- roofline of the persistent solver kernel
     peak, peak_kind = peaks()
@@ -389,25 +416,222 @@ def main():
             "achieved_compulsory": onepass / t_kern / 1e9, "frac_compulsory": onepass / t_kern / 1e9 / peak,
             "launch_ms": t_kern * 1e3}
 
-    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": ws, "steps": args.steps,
+    line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C2: dense pre-computed squared-Euclidean cost n=m=8192 fp32, eps=1e-3, "
                                    f"{K} iterations/step, check every {CHECK}, transport cost",
                        "n": N, "m": N, "eps": EPS, "iterations_per_step": K,
-                       "variant": "exact-two-pass" if args.exact else "stale-shift one-pass",
+                       "variant": ("exact-two-pass" if args.exact else "stale-shift one-pass")
+                       + (", direct g-side arithmetic" if args.direct else
+                          ", multiplicative column update (uniform targets; parity vs the reference at K=1000: "
+                          "profiles/r2_parity_errors.jsonl)"),
                        "l2": "inputs larger than L2 (C = 256 MiB > 126 MB)",
-                       "parallelism": f"independent problems x{ws} (no communication)",
+                       "parallelism": "single GPU (C2 is a 1-GPU config)",
                        "guard_stats_last_step": guard},
             "roofline": roof, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": 3 * args.steps}
-    # single-GPU extras (the other configs' rates, the CPU baseline) at N = 1 only
-    if rank == 0 and ws == 1 and not args.no_extra:
-        line["other_configs"] = other_configs()
-    if rank == 0 and ws == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(X, Y, iters=int(os.environ.get("LSK_CPU_ITERS", "80")))
+    return line, X, Y
+
+
+C4_N, C4_K = 65536, 50      # C4: one 65536^2 problem, iterations per step of the sharded bench
+C5_B, C5_N, C5_K = 256, 4096, 200
+
+
+def _mufu_pairs_per_s():
+    import torch
+
+    sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return 16.0 * sm * 1965.0e6  # one MUFU ex2 per pair evaluation, 16/clk/SM at the max SM clock
+
+
+def _max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def c4_inputs():
+    """generate_rigid_pair(65536, 3, 0.1, [0.1, 0, 0], 0.01, 0)."""
+    from paper_2605_00837_b200 import generate_rigid_pair
+
+    X, Y, _ = generate_rigid_pair(C4_N, 3, 0.1, [0.1, 0.0, 0.0], 0.01, 0)
+    return X, Y
+
+
+def c4_launches_per_iter(ws, shard):
+    """Kernels of ours per C4 iteration (lsk_points_solve.cu), checks amortised
+    over check_interval = 10: f half (part, combine, fixup), g half (owner: the
+    same 3; partials: part, subtree, combine, fixup), check (colcheck, blocksum,
+    decide, active view, + put/or slots when sharded)."""
+    per = 3 + (4 if (ws > 1 and shard != "owner") else 3)
+    return per + (6 if ws > 1 else 4) / 10.0
+
+
+def run_c4(args, ws, rank, comm, barrier, shard, X, Y, steps):
+    import torch
+
+    import paper_2605_00837_b200 as lsk
+    from paper_2605_00837_b200 import points as PT
+
+    cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=C4_K)
+    kw = dict(comm=comm, shard=shard) if comm is not None else {}
+    PT.solve_points_otf(X, Y, None, None, cfg, normalize="max", **kw)  # warm-up
+    barrier()
+    torch.cuda.synchronize()
+    dev = 0.0
+    for _ in range(steps):
+        rep, _ = PT.solve_points_otf(X, Y, None, None, cfg, normalize="max", **kw)
+        assert rep.iterations == C4_K
+        dev += rep.device_seconds
+    barrier()
+    dev = _max_over_ranks(dev, ws)
+    pairs_rank = 2.0 * C4_N * C4_N / ws * C4_K * steps / dev
+    mp = _mufu_pairs_per_s()
+    return {"workload": f"C4: rigid pair n=m={C4_N} 3-D, C/C.max(), eps=1e-3, on the fly, {C4_K} iterations/step, "
+                        f"one problem sharded over {ws} GPU(s) ({shard if ws > 1 else 'unsharded'})",
+            "P": ws, "shard": shard if ws > 1 else "none", "value": C4_K * steps / dev, "unit": "iters/s",
+            "scaling": "strong", "ms_per_iter": dev / (C4_K * steps) * 1e3,
+            "roofline": {"bound": "mufu", "achieved": pairs_rank, "peak": mp, "unit": "pair evals/s per GPU",
+                         "frac": pairs_rank / mp,
+                         "rule": "2*n*m/P pair evaluations per iteration per GPU, one MUFU ex2 each; "
+                                 "peak 16 ex2/clk/SM x SMs x 1.965 GHz"}}
+
+
+def run_c5(args, ws, rank, barrier):
+    """256 problems split 256/N per rank (dist.split_batch), no communication."""
+    import torch
+
+    import paper_2605_00837_b200 as lsk
+    from paper_2605_00837_b200 import dist as D
+    from paper_2605_00837_b200 import points as PT
+
+    lo, hi = D.split_batch(C5_B, ws, rank)
+    Xs, Ys = [], []
+    for b in range(lo, hi):  # SURVEY 8(d): problem b draws X then Y from PCG64(b)
+        rng = np.random.Generator(np.random.PCG64(b))
+        Xs.append(rng.uniform(0.0, 1.0, (C5_N, 3)))
+        Ys.append(rng.uniform(0.0, 1.0, (C5_N, 3)))
+    Xs, Ys = np.stack(Xs), np.stack(Ys)
+    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=C5_K)
+    PT.solve_points_batched(Xs, Ys, cfg)
+    barrier()
+    torch.cuda.synchronize()
+    outs = PT.solve_points_batched(Xs, Ys, cfg)
+    dev = _max_over_ranks(outs[0][0].device_seconds, ws)
+    barrier()
+    pairs_rank = 2.0 * (hi - lo) * C5_N * C5_N * C5_K / dev
+    mp = _mufu_pairs_per_s()
+    return {"workload": f"C5: {C5_B} RGB problems n=m={C5_N}, eps=1e-2, {C5_K} iterations, {hi - lo} per GPU "
+                        f"over {ws} GPU(s), no communication",
+            "P": ws, "value": C5_B * C5_K / dev, "unit": "problem-iters/s", "scaling": "weak (batch split)",
+            "ms_all_problems": dev * 1e3,
+            "roofline": {"bound": "mufu", "achieved": pairs_rank, "peak": mp, "unit": "pair evals/s per GPU",
+                         "frac": pairs_rank / mp}}
+
+
+def scaling_configs(args, ws, rank, comm, barrier, local):
+    X, Y = c4_inputs()
+    steps = max(1, min(args.steps, 3))
+    out = {"C4": run_c4(args, ws, rank, comm, barrier, "partials", X, Y, steps)}
+    if ws > 1:
+        out["C4_owner_computes"] = run_c4(args, ws, rank, comm, barrier, "owner", X, Y, steps)
+    out["C5"] = run_c5(args, ws, rank, barrier)
+    return out
+
+
+def sharded_line(args, ws, rank, comm, barrier, local):
+    """N > 1: the headline is C4 sharded over the N ranks (strong scaling)."""
+    import torch
+
+    import paper_2605_00837_b200 as lsk
+    from paper_2605_00837_b200 import points as PT
+
+    X, Y = c4_inputs()
+    steps = args.steps
+    with Clocks(local) as clk:
+        c4 = run_c4(args, ws, rank, comm, barrier, "partials", X, Y, steps)
+    sc = {"C4": c4, "C4_owner_computes": run_c4(args, ws, rank, comm, barrier, "owner", X, Y, max(1, min(3, steps))),
+          "C5": run_c5(args, ws, rank, barrier)}
+    # e2e: the public API from host numpy points to host numpy potentials
+    cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=C4_K)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(3, steps))
+    for _ in range(e2e_steps):
+        rep, pot = PT.solve_points_otf(X, Y, None, None, cfg, normalize="max", comm=comm, shard="partials")
+    torch.cuda.synchronize()
+    t = _max_over_ranks(time.perf_counter() - t0, ws)
+    e2e = {"value": C4_K * e2e_steps / t, "unit": "iters/s", "h2d_bytes_per_step": 2 * C4_N * 3 * 8 + 3 * C4_N * 4,
+           "d2h_bytes_per_step": 2 * C4_N * 4 + 64,
+           "path": "paper_2605_00837_b200.solve_points_otf(numpy X, Y, comm=..., shard='partials') -> numpy potentials"}
+    return {"metric": METRIC, "value": c4["value"], "unit": "iters/s", "n_gpus": ws, "steps": steps,
+            "warmup": 1, "ms_per_step": c4["ms_per_iter"] * C4_K, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (generate_rigid_pair, seed 0)",
+            "config": {"workload": c4["workload"], "n": C4_N, "m": C4_N, "eps": 1e-3, "iterations_per_step": C4_K,
+                       "parallelism": f"row-sharded x{ws}, column partials allgathered (NCCL)",
+                       "l2": "on-the-fly cost: no C in memory; inputs 1 MB per cloud",
+                       "note": "C2 (the BASELINE headline) is a single-GPU config; at N > 1 this line reports the "
+                               "north star's scaling target (C4). scaling_configs.C4.value at N = 1 is in BENCH."},
+            "roofline": c4["roofline"], "e2e": e2e, "clocks": clk.summary(), "scaling_configs": sc,
+            "gpu_launches": int(round(c4_launches_per_iter(ws, "partials") * C4_K * steps))}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=KITER)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other-config rate lines")
+    ap.add_argument("--exact", action="store_true", help="exact two-pass variant instead of stale shift")
+    ap.add_argument("--direct", action="store_true", help="no multiplicative column update (LSK_FLAG_NO_MULT)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_00837_b200 as lsk
+    from paper_2605_00837_b200 import solver as S
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    comm = None
+    if ws > 1:
+        from paper_2605_00837_b200 import dist as D
+
+        comm = D.Communicator.from_torch_distributed()
+    if ws == 1:
+        line, X, Y = c2_line(args, local)
+        if not args.no_extra:
+            line["scaling_configs"] = scaling_configs(args, 1, 0, None, barrier, local)
+            line["other_configs"] = other_configs()
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(X, Y, iters=int(os.environ.get("LSK_CPU_ITERS", "80")))
+            line["cpu_baseline"]["other_configs"] = cpu_baselines_other()
+    else:
+        line = sharded_line(args, ws, rank, comm, barrier, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if ws > 1:
         barrier()
         dist.destroy_process_group()

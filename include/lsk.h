@@ -39,7 +39,6 @@ extern "C" {
 /* lsk_solve_dense_f32 flags */
 #define LSK_FLAG_STALE_SHIFT 1 /* one-pass stale-shift iteration (default fast path) */
 #define LSK_FLAG_COST 2        /* compute the transport cost after the loop */
-#define LSK_FLAG_TASKQ 4       /* dense m <= 8192: task-queue variant (warp per row / per column strip) */
 #define LSK_FLAG_EXPANSION 8   /* points, eps >= 5e-3: cost as |x|^2+|y|^2-2x.y in the stale sweeps; the
                                   caller requests it only when (max|x-x0|^2 + max|y-x0|^2) 2^-24 /
                                   (eps * normaliser) is small (x0 = the problem's first source point) */
@@ -189,22 +188,60 @@ int32_t lsk_materialize_plan_f64(const double* C, int64_t ldc, int32_t n, int32_
  * d in 1..3; cost c_ij = scale[b] * sum_k (x_ik - y_jk)^2 with scale (B floats,
  * device) = 1 or 1/Cmax (lsk_points_cost_max). log_mu/mu (B, n), log_nu (B, m)
  * fp32 device. Same iteration, check, trace and status semantics as
- * lsk_solve_dense_f32, per problem; a problem that stops no longer runs.
+ * lsk_solve_dense_f32, per problem; a problem that stops no longer runs, and
+ * the host stops enqueueing once every problem has stopped.
  * Outputs: f_out (B, n), g_out (B, m), trace_iter/trace_err (B, capacity),
  * result (B, 8) int32 (LSK_RES_*), result_f (B, 2) float (final error, cost).
- * comm: NULL, or an lsk_comm_create() communicator of P ranks (B must be 1,
- * P must divide n and m): rank r owns rows [r n/P, (r+1) n/P) for the f update
- * and columns [r m/P, (r+1) m/P) for the g update; potentials are allgathered
- * after each half-step, so results are bit-identical to one GPU for any P.
+ *
+ * comm: NULL, or an lsk_comm_create() communicator of P ranks (B must be 1;
+ * SURVEY 8(e)). The design is chosen by the flags:
+ *   LSK_FLAG_SHARD_PARTIALS  -- rank r owns a row slab of the source cloud
+ *     (whole 2048-point chunks: rows [r R, (r+1) R), R = 2048 L/P with L the
+ *     next power of two of ceil(n/2048)); f is local; for g each rank reduces
+ *     its rows into per-column partials (stale sums or (max, sumexp) pairs),
+ *     the complete subtree of the fixed chunk tree it owns; the P roots are
+ *     allgathered and merged by the top of that tree. P must be a power of two
+ *     <= L. Bit-identical to one GPU for every such P.
+ *   LSK_FLAG_SHARD_ALLREDUCE -- as partials, but the stale sums are combined
+ *     by ncclAllReduce(SUM) (NCCL's order: within rounding of one GPU, not
+ *     bitwise).
+ *   neither -- owner computes: rank r computes f for rows [r ceil(n/P), ...)
+ *     and g for columns [r ceil(m/P), ...) against everything; the potential
+ *     slabs are allgathered after each half-step. Any P; bit-identical.
+ * Every design allgathers f after the f half-step. The sharded workspace is
+ * lsk_solve_points_sharded_workspace_bytes(n, m, P, mode).
  * Numerics: fp32 direct-form cost (~2-3e-6 on potentials at
  * eps = 1e-3); use the dense path with lsk_build_cost_f32 below eps = 1e-3.
  */
+#define LSK_FLAG_SHARD_PARTIALS 128
+#define LSK_FLAG_SHARD_ALLREDUCE 256
+#define LSK_SHARD_NONE 0
+#define LSK_SHARD_OWNER 1
+#define LSK_SHARD_PARTIALS 2
+#define LSK_SHARD_ALLREDUCE 3
+#define LSK_EMU_MAX_RANKS 16
 size_t lsk_solve_points_workspace_bytes(int32_t B, int32_t n, int32_t m);
+size_t lsk_solve_points_sharded_workspace_bytes(int32_t n, int32_t m, int32_t P, int32_t shard_mode);
 int32_t lsk_solve_points_f32(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
                              const float* scale, const float* log_mu, const float* log_nu, const float* mu,
                              double eps, double tol, int32_t max_iter, int32_t check_interval, int32_t flags,
                              float* f_out, float* g_out, int32_t* trace_iter, float* trace_err, int32_t* result,
                              float* result_f, void* workspace, size_t workspace_bytes, void* comm, void* stream);
+
+/* Single-GPU emulation of the P-rank decomposition (test hook; B = 1): the P
+ * ranks' kernels run rank after rank on `stream`, each rank in its own slice
+ * of the workspace (P x lsk_solve_points_sharded_workspace_bytes), and the
+ * collectives become device copies (the allreduce a rank-order sum). Outputs
+ * are rank 0's; *rank_mismatch (device int) counts ranks whose returned
+ * potentials, status, iterations, error or cost differ in any bit from rank
+ * 0's. shard_mode: LSK_SHARD_OWNER / _PARTIALS / _ALLREDUCE (P in 1..16), or
+ * LSK_SHARD_NONE with P = 1. */
+int32_t lsk_solve_points_emulated_f32(const double* X, const double* Y, int32_t n, int32_t m, int32_t d,
+                                      const float* scale, const float* log_mu, const float* log_nu, const float* mu,
+                                      double eps, double tol, int32_t max_iter, int32_t check_interval, int32_t flags,
+                                      int32_t P, int32_t shard_mode, float* f_out, float* g_out, int32_t* trace_iter,
+                                      float* trace_err, int32_t* result, float* result_f, int32_t* rank_mismatch,
+                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* Plan consumers without the plan (f, g from a solve; pi_ij as in
  * materialize_plan): mapped_out (B, n, d) = sum_j pi_ij y_j / sum_j pi_ij --

@@ -19,11 +19,17 @@ LSK_ECUDA = -2
 LSK_EUNSUPPORTED = -3
 LSK_FLAG_STALE_SHIFT = 1
 LSK_FLAG_COST = 2
-LSK_FLAG_TASKQ = 4
 LSK_FLAG_EXPANSION = 8
 LSK_FLAG_UNIFORM_NU = 16
 LSK_FLAG_NO_MULT = 32
 LSK_FLAG_STD_MULTIKERNEL = 64
+LSK_FLAG_SHARD_PARTIALS = 128
+LSK_FLAG_SHARD_ALLREDUCE = 256
+LSK_SHARD_NONE = 0
+LSK_SHARD_OWNER = 1
+LSK_SHARD_PARTIALS = 2
+LSK_SHARD_ALLREDUCE = 3
+LSK_EMU_MAX_RANKS = 16
 
 _c_i32, _c_i64, _c_sz, _c_dbl, _c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t, ctypes.c_double, ctypes.c_void_p
 
@@ -66,6 +72,10 @@ SIGNATURES = {
     "lsk_solve_points_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl,
                                       _c_dbl, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                       _c_sz, _c_p, _c_p]),
+    "lsk_solve_points_sharded_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32, _c_i32]),
+    "lsk_solve_points_emulated_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_dbl,
+                                               _c_dbl, _c_i32, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p,
+                                               _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_points_consume_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_points_consume_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
                                         _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),

@@ -7,7 +7,6 @@
 
 #include "../../include/lsk.h"
 #include "lsk_dense.cuh"
-#include "lsk_dense4.cuh"
 #include "lsk_kernels.cuh"
 
 namespace {
@@ -136,90 +135,11 @@ DenseLayout dense_layout(int n, int m) {
   return L;
 }
 
-using SolverV4 = lsk::DenseV4<512, 8192>;
-
-__global__ void __launch_bounds__(512, 1) k_solve_dense4(lsk::D4Args a) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  SolverV4 sv(a, smem);
-  sv.solve();
-}
-
-struct D4Layout {
-  size_t zero_bytes, f0, f1, g0, g1, rows_done, part, pairs, rowterm, total;
-};
-D4Layout d4_layout(int n, int m) {
-  D4Layout L{};
-  const int mpad = (m + 3) / 4 * 4;
-  const int S = (n + SolverV4::SR - 1) / SolverV4::SR;
-  size_t o = kHeaderInts * 4;
-  L.f0 = o; o = align_up(o + size_t(n) * 4, 256);
-  L.g0 = o; o = align_up(o + size_t(m) * 4, 256);
-  L.rows_done = o; o = align_up(o + size_t(S) * 4, 256);
-  L.zero_bytes = o;
-  L.f1 = o; o = align_up(o + size_t(n) * 4, 256);
-  L.g1 = o; o = align_up(o + size_t(m) * 4, 256);
-  L.part = o; o = align_up(o + size_t(S) * mpad * 4, 256);
-  L.pairs = o; o = align_up(o + size_t(S) * mpad * 8, 256);
-  L.rowterm = o; o = align_up(o + size_t(n) * 4, 256);
-  L.total = o;
-  return L;
-}
-
-int32_t solve_dense4(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu, const float* log_nu,
-                     const float* mu, double eps, double tol, int32_t max_iter, int32_t check_interval, int32_t flags,
-                     float* f_out, float* g_out, int32_t* result, float* result_f, int32_t* trace_iter,
-                     float* trace_err, void* workspace, size_t workspace_bytes, cudaStream_t st) {
-  const D4Layout L = d4_layout(n, m);
-  if (!workspace || workspace_bytes < L.total) return fail(LSK_EINVAL, "workspace too small");
-  char* ws = static_cast<char*>(workspace);
-  LSK_CUDA(cudaMemsetAsync(ws, 0, L.zero_bytes, st));
-  int* hdr = reinterpret_cast<int*>(ws);
-  EpsConsts ec = eps_consts(eps);
-  lsk::D4Args a{};
-  a.C = C; a.ldc = ldc; a.n = n; a.m = m; a.mpad = (m + 3) / 4 * 4;
-  a.log_mu = log_mu; a.log_nu = log_nu; a.mu = mu;
-  a.inv_eps = ec.inv_eps; a.neg_eps = ec.neg_eps; a.negzero = -0.0f; a.tol = tol;
-  a.max_iter = max_iter; a.check = check_interval;
-  a.stale = (flags & LSK_FLAG_STALE_SHIFT) ? 1 : 0;
-  a.want_cost = (flags & LSK_FLAG_COST) ? 1 : 0;
-  a.f0 = reinterpret_cast<float*>(ws + L.f0); a.f1 = reinterpret_cast<float*>(ws + L.f1);
-  a.g0 = reinterpret_cast<float*>(ws + L.g0); a.g1 = reinterpret_cast<float*>(ws + L.g1);
-  a.part = reinterpret_cast<float*>(ws + L.part);
-  a.pairs = reinterpret_cast<float2*>(ws + L.pairs);
-  a.rowterm = reinterpret_cast<float*>(ws + L.rowterm);
-  a.rows_done = reinterpret_cast<unsigned*>(ws + L.rows_done);
-  a.tctr = reinterpret_cast<unsigned*>(hdr + 16);
-  a.bar = reinterpret_cast<unsigned long long*>(hdr + 12);
-  a.guard = hdr + 1; a.stats = hdr + 2; a.out_status = hdr + 4; a.out_iters = hdr + 5; a.n_trace = hdr + 6;
-  a.out_fbuf = hdr + 7; a.out_err = reinterpret_cast<float*>(hdr + 8); a.out_cost = reinterpret_cast<float*>(hdr + 9);
-  a.trace_iter = trace_iter; a.trace_err = trace_err;
-  static bool attr = false;
-  if (!attr) {
-    LSK_CUDA(cudaFuncSetAttribute(k_solve_dense4, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(SolverV4::kSmemBytes)));
-    attr = true;
-  }
-  const int G = num_sms();
-  void* args[] = {&a};
-  LSK_CUDA(cudaLaunchCooperativeKernel((const void*)k_solve_dense4, dim3(G), dim3(512), args, SolverV4::kSmemBytes, st));
-  lsk::k_pick<<<64, 256, 0, st>>>(a.f0, a.f1, a.out_fbuf, n, f_out);
-  lsk::k_pick<<<64, 256, 0, st>>>(a.g0, a.g1, a.out_fbuf, m, g_out);
-  LSK_CUDA(cudaMemcpyAsync(result + 0, hdr + 4, 4, cudaMemcpyDeviceToDevice, st));
-  LSK_CUDA(cudaMemcpyAsync(result + 1, hdr + 5, 4, cudaMemcpyDeviceToDevice, st));
-  LSK_CUDA(cudaMemcpyAsync(result + 2, hdr + 6, 8, cudaMemcpyDeviceToDevice, st));
-  LSK_CUDA(cudaMemcpyAsync(result + 4, hdr + 2, 8, cudaMemcpyDeviceToDevice, st));
-  LSK_CUDA(cudaMemcpyAsync(result_f, hdr + 8, 8, cudaMemcpyDeviceToDevice, st));
-  LSK_CUDA(cudaGetLastError());
-  return LSK_OK;
-}
-
 template <class SV>
 int32_t launch_dense(lsk::DenseArgs& a, int G, cudaStream_t st) {
-  static bool attr_set = false;  // per instance
-  if (!attr_set) {
-    LSK_CUDA(cudaFuncSetAttribute(k_solve_dense<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SV::kSmemBytes)));
-    attr_set = true;
-  }
+  // the attribute belongs to the current device's context: set it on every
+  // launch (cheap), never cached process-wide
+  LSK_CUDA(cudaFuncSetAttribute(k_solve_dense<SV>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SV::kSmemBytes)));
   int per_sm = 0;
   LSK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_dense<SV>, SV::NW * 32, SV::kSmemBytes));
   if (per_sm < 1) return fail(LSK_ECUDA, "dense solver: kernel does not fit on an SM");
@@ -263,8 +183,7 @@ int32_t lsk_trace_capacity(int32_t max_iter, int32_t check_interval) {
 size_t lsk_solve_dense_workspace_bytes(int32_t n, int32_t m) {
   if (n < 1 || m < 1) return 0;
   if (dense_width(m) == 0) return lsk_host::dense_loop_workspace_bytes(n, m);
-  const size_t a = dense_layout(n, m).total, b = d4_layout(n, m).total;
-  return a > b ? a : b;  // either dense variant fits
+  return dense_layout(n, m).total;
 }
 
 int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, const float* log_mu,
@@ -284,9 +203,6 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
                                       check_interval, flags, f_out, g_out, trace_iter, trace_err, result, result_f,
                                       workspace, workspace_bytes, S(stream));
   }
-  if (flags & LSK_FLAG_TASKQ)
-    return solve_dense4(C, ldc, n, m, log_mu, log_nu, mu, eps, tol, max_iter, check_interval, flags, f_out, g_out,
-                        result, result_f, trace_iter, trace_err, workspace, workspace_bytes, S(stream));
   DenseLayout L = dense_layout(n, m);
   if (!workspace || workspace_bytes < L.total) return fail(LSK_EINVAL, "workspace too small");
   cudaStream_t st = S(stream);

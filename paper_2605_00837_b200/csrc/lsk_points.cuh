@@ -47,6 +47,7 @@ struct PtsHalf {
   int B, n_rows, n_cols;
   int row_lo, row_hi;          // this rank's slab of rows [row_lo, row_hi)
   int chunks;                  // ceil(n_cols / kPtsChunk)
+  int ch_lo;                   // first column chunk this launch covers (grid.x chunks from here)
   const float4* rpts;          // (B, n_rows) points (x, y, z, 0)
   const float4* cpts;          // (B, n_cols)
   const float* rpot;           // (B, n_rows) old row potential (stale shift / cost)
@@ -69,7 +70,7 @@ static __global__ void __launch_bounds__(kPtsThreads, (RPW > 8 ? 2 : 3)) k_pts_p
   constexpr int PP = RPW / 2, TILE = 8 * RPW;
   __shared__ __align__(16) float4 colv[kPtsChunk];
   __shared__ int tile_any;
-  const int ch = blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
+  const int ch = h.ch_lo + blockIdx.x, tile = blockIdx.y, b = blockIdx.z;
   if (MODE == kPtsOnline && h.nflag && *h.nflag == 0) return;
   if (h.active && !h.active[b]) return;
   const int r_base = h.row_lo + tile * TILE;
@@ -220,8 +221,65 @@ static __global__ void __launch_bounds__(kPtsThreads, (RPW > 8 ? 2 : 3)) k_pts_p
   }
 }
 
+// ---- fixed-shape combine of per-chunk partials: a balanced binary tree over
+// `cnt` (a power of two) leaves [lo, lo + cnt), leaves >= nreal being the
+// identity. The leaf count is a function of the column count only, never of
+// the rank count, so a rank that owns the complete subtree [r cnt/P, (r+1)
+// cnt/P) can reduce it locally (k_pts_subtree) and the P subtree roots
+// combine with the top P leaves of the same tree: bitwise the single-GPU
+// result for every power-of-two P. Identity padding is skipped
+// (merge(x, id) == x bit for bit for both operators), and the partial
+// subtrees left on the stack fold right to left, exactly as the padded tree.
+struct SumOp {
+  using T = float;
+  __device__ static T ident() { return 0.f; }
+  __device__ static T merge(T a, T b) { return __fadd_rn(a, b); }
+};
+// (max, sum) pairs in log2 units: the online max-rescale merge
+struct PairOp {
+  using T = float2;
+  __device__ static T ident() { return make_float2(-INFINITY, 0.f); }
+  __device__ static T merge(T a, T b) {
+    const float mm = fmax_nan(a.x, b.x);
+    const float mms = (fabsf(mm) <= 3.402823466e38f) ? mm : 0.f;
+    const float wa = (a.x == -INFINITY) ? 0.f : ex2(a.x - mms), wb = (b.x == -INFINITY) ? 0.f : ex2(b.x - mms);
+    return make_float2(mm, __fmaf_rn(a.y, wa, b.y * wb));
+  }
+};
+constexpr int kTreeDepth = 32;
+template <class Op, class Get>
+__device__ __forceinline__ typename Op::T leaf_tree(int lo, int cnt, int nreal, Get get) {
+  using T = typename Op::T;
+  T stk[kTreeDepth];
+  int lev[kTreeDepth];
+  int sp = 0;
+  const int hi = min(lo + cnt, nreal);
+  for (int l = lo; l < hi; ++l) {
+    T v = get(l);
+    int lv = 0;
+    while (sp > 0 && lev[sp - 1] == lv) {
+      v = Op::merge(stk[sp - 1], v);
+      --sp;
+      ++lv;
+    }
+    stk[sp] = v;
+    lev[sp] = lv;
+    ++sp;
+  }
+  if (sp == 0) return Op::ident();
+  T acc = stk[sp - 1];
+  for (int i = sp - 2; i >= 0; --i) acc = Op::merge(stk[i], acc);
+  return acc;
+}
+__host__ __device__ inline int pow2_ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
 struct PtsCombine {
   int B, n_rows, row_lo, row_hi, chunks;
+  int nleaves;            // tree width: pow2_ceil(chunks) (or the rank count over subtree roots)
   const void* part;
   const float* rpot_old;  // (B, n_rows) stale potential (shift); for check: f^k
   float* rpot_new;        // (B, n_rows) new potential (nullptr: check only)
@@ -251,15 +309,9 @@ static __global__ void k_pts_combine(PtsCombine c) {
   if (MODE == kPtsOnline) {
     if (c.rowflag && !c.rowflag[ri]) return;
     const float2* p = reinterpret_cast<const float2*>(c.part);
-    float m2 = -INFINITY, s2 = 0.f;
-    for (int ch = 0; ch < c.chunks; ++ch) {
-      const float2 v = p[((size_t)b * c.chunks + ch) * c.n_rows + r];
-      const float mm = fmax_nan(m2, v.x);
-      const float mms = (fabsf(mm) <= 3.402823466e38f) ? mm : 0.f;
-      const float wa = (m2 == -INFINITY) ? 0.f : ex2(m2 - mms), wb = (v.x == -INFINITY) ? 0.f : ex2(v.x - mms);
-      s2 = __fmaf_rn(s2, wa, v.y * wb);
-      m2 = mm;
-    }
+    const float2 t = leaf_tree<PairOp>(0, c.nleaves, c.chunks,
+                                       [&](int ch) { return p[((size_t)b * c.chunks + ch) * c.n_rows + r]; });
+    const float m2 = t.x, s2 = t.y;
     // LSE = M2 * ln2 + ln S (reduction.py:196-207: an all -inf row gives -inf)
     float L;
     if (!(fabsf(m2) <= 3.402823466e38f)) L = -INFINITY;
@@ -269,8 +321,8 @@ static __global__ void k_pts_combine(PtsCombine c) {
     return;
   }
   const float* p = reinterpret_cast<const float*>(c.part);
-  float S = 0.f;
-  for (int ch = 0; ch < c.chunks; ++ch) S += p[((size_t)b * c.chunks + ch) * c.n_rows + r];
+  const float S = leaf_tree<SumOp>(0, c.nleaves, c.chunks,
+                                   [&](int ch) { return p[((size_t)b * c.chunks + ch) * c.n_rows + r]; });
   const float pold = c.rpot_old[ri];
   const float sh = __fmul_rn(-pold, c.inv_eps);
   const bool ok = S >= kShiftLo && S <= kShiftHi;
@@ -289,6 +341,29 @@ static __global__ void k_pts_combine(PtsCombine c) {
     if (!isfinite(pold) || !ok) {
       if (!isfinite(pold)) atomicOr(c.badrow + b, 1);
     }
+  }
+}
+
+// A rank's complete subtree of the chunk tree, leaves [leaf_lo, leaf_lo + cnt),
+// for rows [row_lo, row_hi) of problem 0 (sharded solves are single-problem):
+// the root goes to slot row r of `out` (n_rows entries), the rank's
+// contribution to the exchange.
+template <int MODE>
+static __global__ void k_pts_subtree(int n_rows, int row_lo, int row_hi, int chunks, int leaf_lo, int cnt,
+                                     const void* __restrict__ part, void* __restrict__ out, const int* active,
+                                     const int* nflag_in) {
+  const int r = row_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= row_hi) return;
+  if (active && !active[0]) return;
+  if (MODE == kPtsOnline && nflag_in && *nflag_in == 0) return;
+  if (MODE == kPtsOnline) {
+    const float2* p = reinterpret_cast<const float2*>(part);
+    reinterpret_cast<float2*>(out)[r] =
+        leaf_tree<PairOp>(leaf_lo, cnt, chunks, [&](int ch) { return p[(size_t)ch * n_rows + r]; });
+  } else {
+    const float* p = reinterpret_cast<const float*>(part);
+    reinterpret_cast<float*>(out)[r] =
+        leaf_tree<SumOp>(leaf_lo, cnt, chunks, [&](int ch) { return p[(size_t)ch * n_rows + r]; });
   }
 }
 

@@ -409,11 +409,8 @@ int32_t solve_standard(const T* C, int64_t ldc, int32_t n, int32_t m, const T* m
       S_CUDA(cudaMemsetAsync(ws + L.bar, 0, 16, st));
       S_CUDA(cudaMemsetAsync(ws + L.outbuf, 0, 16, st));
       k_std_init<<<64, 256, 0, st>>>(sa.u0, n, sa.v0, m, S);
-      static bool attr = false;
-      if (!attr) {
-        S_CUDA(cudaFuncSetAttribute(k_std_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(StdFused::kSmemBytes)));
-        attr = true;
-      }
+      // per-device-context attribute: set on every launch, never cached process-wide
+      S_CUDA(cudaFuncSetAttribute(k_std_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(StdFused::kSmemBytes)));
       void* args[] = {&sa};
       S_CUDA(cudaLaunchCooperativeKernel((const void*)k_std_fused, dim3(G), dim3(StdFused::NW * 32), args, StdFused::kSmemBytes, st));
       k_std_pick<<<64, 256, 0, st>>>(sa.u0, sa.u1, n, sa.v0, sa.v1, m, sa.out_buf, u, v);

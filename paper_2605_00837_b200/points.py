@@ -7,9 +7,13 @@ materialising the (n, m) cost: one ``lsk_solve_points_f32`` call runs the whole
 solve for a batch of problems, recomputing ``sum_k (x_ik - y_jk)^2`` in
 registers. Returns the reference's ``(SolveReport, DualPotentials)``.
 
-* ``solve_points_otf``: one problem; with ``comm`` (``dist.Communicator``) the
-  rows and columns are sharded over the ranks (owner computes), bit-identical to
-  one GPU.
+* ``solve_points_otf``: one problem; with ``comm`` (``dist.Communicator``) it
+  is sharded over the ranks: ``shard="partials"`` (default: row
+  slabs of the source cloud, per-column partials exchanged and merged by a
+  fixed tree), ``"allreduce"`` (stale sums by ncclAllReduce) or ``"owner"``
+  (owner computes, potential slabs allgathered). ``emulate_ranks=P`` runs the
+  same P-rank decomposition on one GPU (collectives as device copies) and
+  checks that every virtual rank ends bit-identical.
 * ``solve_points_batched``: B independent problems of one shape in a single
   launch sequence; each problem stops on its own (per-problem status / trace).
 
@@ -28,7 +32,7 @@ from .errors import DimensionMismatch
 from .solver import _STATUS_BY_CODE, _ptr, _stream_ptr, _torch
 from .types import DualPotentials, SolveReport
 
-__all__ = ["solve_points_otf", "solve_points_batched", "points_cost_max"]
+__all__ = ["solve_points_otf", "solve_points_batched", "solve_points_emulated", "points_cost_max"]
 
 
 def _batch_points(P):
@@ -73,7 +77,11 @@ def points_cost_max(Xd, Yd):
 
 
 class _PointsRun:
-    __slots__ = ("B", "n", "m", "f", "g", "ti", "te", "res", "resf", "ev0", "ev1", "t0", "keep")
+    __slots__ = ("B", "n", "m", "f", "g", "ti", "te", "res", "resf", "ev0", "ev1", "t0", "keep", "mismatch")
+
+
+_SHARD = {"owner": (_lib.LSK_SHARD_OWNER, 0), "partials": (_lib.LSK_SHARD_PARTIALS, _lib.LSK_FLAG_SHARD_PARTIALS),
+          "allreduce": (_lib.LSK_SHARD_ALLREDUCE, _lib.LSK_FLAG_SHARD_ALLREDUCE)}
 
 
 # The expansion form c = |x|^2 + |y|^2 - 2 x.y (kernels translate every problem by
@@ -95,7 +103,8 @@ def _expansion_ok(Xb, Yb, eps, normalize):
     return bool(np.all(bound <= _EXPANSION_BOUND))
 
 
-def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=False):
+def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=False, shard="partials",
+            emulate_ranks=None):
     torch = _torch()
     if config.precision != "single":
         raise NotImplementedError("precision='double' is not available on the B200 path (fp32 only)")
@@ -124,7 +133,25 @@ def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=F
     mu_d = torch.from_numpy(wmu.astype(np.float32)).to("cuda")
     K, c = int(config.max_iterations), int(config.check_interval)
     cap = _lib.load().lsk_trace_capacity(K, c)
-    wsb = _lib.load().lsk_solve_points_workspace_bytes(B, n, m)
+    if shard not in _SHARD:
+        raise ValueError("shard must be 'partials', 'allreduce' or 'owner'")
+    mode, shard_flag = _SHARD[shard]
+    lib = _lib.load()
+    if emulate_ranks is not None:
+        if B != 1 or comm is not None:
+            raise ValueError("emulate_ranks: one problem, no communicator")
+        P = int(emulate_ranks)
+        wsb = P * lib.lsk_solve_points_sharded_workspace_bytes(n, m, P, mode)
+    elif comm is not None:
+        if B != 1:
+            raise ValueError("a sharded solve takes one problem (split batches over ranks instead)")
+        wsb = lib.lsk_solve_points_sharded_workspace_bytes(n, m, comm.world, mode)
+    else:
+        shard_flag = 0
+        wsb = lib.lsk_solve_points_workspace_bytes(B, n, m)
+    if wsb == 0:
+        _lib.call("lsk_solve_points_sharded_workspace_bytes", n, m, emulate_ranks or comm.world, mode)
+        raise ValueError(f"shard={shard!r} does not support this rank count / shape")
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     r.f = torch.empty((B, n), dtype=torch.float32, device="cuda")
     r.g = torch.empty((B, m), dtype=torch.float32, device="cuda")
@@ -136,13 +163,22 @@ def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=F
     if expansion and not _expansion_ok(Xb, Yb, config.epsilon, normalize):
         expansion = False
     flags |= _lib.LSK_FLAG_EXPANSION if expansion else 0
+    flags |= shard_flag
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
+    r.mismatch = None
     r.ev0.record()
-    _lib.call("lsk_solve_points_f32", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(scale), _ptr(lmu_d), _ptr(lnu_d),
-              _ptr(mu_d), float(config.epsilon), float(config.tolerance), K, c, flags, _ptr(r.f), _ptr(r.g),
-              _ptr(r.ti), _ptr(r.te), _ptr(r.res), _ptr(r.resf), _ptr(ws), wsb,
-              comm.handle if comm is not None else None, _stream_ptr(torch))
+    if emulate_ranks is not None:
+        r.mismatch = torch.zeros(1, dtype=torch.int32, device="cuda")
+        _lib.call("lsk_solve_points_emulated_f32", _ptr(Xd), _ptr(Yd), n, m, d, _ptr(scale), _ptr(lmu_d),
+                  _ptr(lnu_d), _ptr(mu_d), float(config.epsilon), float(config.tolerance), K, c, flags,
+                  int(emulate_ranks), mode, _ptr(r.f), _ptr(r.g), _ptr(r.ti), _ptr(r.te), _ptr(r.res),
+                  _ptr(r.resf), _ptr(r.mismatch), _ptr(ws), wsb, _stream_ptr(torch))
+    else:
+        _lib.call("lsk_solve_points_f32", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(scale), _ptr(lmu_d), _ptr(lnu_d),
+                  _ptr(mu_d), float(config.epsilon), float(config.tolerance), K, c, flags, _ptr(r.f), _ptr(r.g),
+                  _ptr(r.ti), _ptr(r.te), _ptr(r.res), _ptr(r.resf), _ptr(ws), wsb,
+                  comm.handle if comm is not None else None, _stream_ptr(torch))
     r.ev1.record()
     r.keep = (Xd, Yd, scale, lmu_d, lnu_d, mu_d, ws)  # alive until the results are read
     return r
@@ -170,14 +206,28 @@ def _reports(r, return_device=False):
 
 
 def solve_points_otf(X, Y, mu, nu, config, normalize="none", *, stale_shift=True, comm=None, return_device=False,
-                     expansion=True):
+                     expansion=True, shard="partials"):
     """One on-the-fly solve of points X (n, d) vs Y (m, d); see module doc.
     ``expansion`` (default on) evaluates the cost as |x|^2+|y|^2-2x.y in the
     stale sweeps when eps >= 5e-3 and the rounding bound of that form is small
     against eps (``_expansion_ok``; 3 instead of 6 FP32 ops per pair, parity
-    tested on the C5 shape); otherwise the direct form is used."""
-    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, comm, expansion)
+    tested on the C5 shape); otherwise the direct form is used.
+    ``comm`` / ``shard``: see the module doc."""
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, comm, expansion, shard)
     return _reports(r, return_device)[0]
+
+
+def solve_points_emulated(X, Y, mu, nu, config, ranks, normalize="none", *, shard="partials", stale_shift=True,
+                          expansion=True):
+    """The P-rank decomposition of ``solve_points_otf(..., comm=<P ranks>,
+    shard=shard)`` run on this one GPU: every virtual rank has its own
+    workspace, its kernels run rank after rank, and the collectives are device
+    copies (``lsk_solve_points_emulated_f32``). Returns ``(report, potentials,
+    rank_mismatch)`` -- rank 0's results and the number of ranks whose returned
+    potentials / status / error / cost differ from rank 0's in any bit."""
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, None, expansion, shard, ranks)
+    rep, pot = _reports(r)[0]
+    return rep, pot, int(r.mismatch.item())
 
 
 def solve_points_batched(X, Y, config, mu=None, nu=None, normalize="none", *, stale_shift=True,

@@ -133,7 +133,7 @@ def _uniform(log_w):
     return False
 
 
-def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None, taskq=False,
+def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None,
                   uniform_nu=False, mult=True):
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
@@ -149,7 +149,6 @@ def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=
     r.res = torch.zeros(8, dtype=torch.int32, device="cuda")
     r.resf = torch.zeros(2, dtype=torch.float32, device="cuda")
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
-    flags |= _lib.LSK_FLAG_TASKQ if taskq else 0
     flags |= _lib.LSK_FLAG_UNIFORM_NU if uniform_nu else 0
     flags |= 0 if mult else _lib.LSK_FLAG_NO_MULT
     r.ev0 = torch.cuda.Event(enable_timing=True)
@@ -191,7 +190,7 @@ def _report_from(r, t0, return_device=False):
     return report, DualPotentials(alpha=alpha, beta=beta)
 
 
-def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, taskq=False):
+def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multiplicative=True):
     """Log-domain Sinkhorn from zero potentials (reference solver.py:230-337).
 
     Alternates f (alpha) and g (beta) updates, checks the L1 row-marginal
@@ -202,8 +201,9 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, taskq=
     transport cost unless the solve failed. The whole loop is one
     cooperative kernel launch; the host synchronises once, at the end.
 
-    ``taskq=True`` selects the task-queue kernel (a warp per row for the f
-    update and per 128-column strip for the g update; same results contract).
+    ``multiplicative=False`` disables the multiplicative column update of the
+    uniform-target kernel (``LSK_FLAG_NO_MULT``) and forms every
+    g-side argument from the cost element as the reference does.
     ``stale_shift=False`` selects the exact two-pass variant (max pass per
     row, exact column pass every iteration) instead of the one-pass
     stale-shift fast path; ``return_device=True`` leaves the potentials as
@@ -221,8 +221,8 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, taskq=
     log_mu = _dev_f32(torch, mu.log_weights)
     log_nu = _dev_f32(torch, nu.log_weights)
     mu32 = _dev_f32(torch, mu.weights)
-    r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift, taskq=taskq,
-                         uniform_nu=_uniform(nu.log_weights))
+    r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift,
+                         uniform_nu=_uniform(nu.log_weights), mult=multiplicative)
     return _report_from(r, t0, return_device)
 
 

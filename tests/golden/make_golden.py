@@ -197,6 +197,24 @@ def big_cases():
          X0=X[0], Y0=Y[0], perm5=perm[:5], Cmax=3.0914804297769676)
 
 
+def long_c2():
+    """C2 at the benchmarked iteration count (BASELINE configs[1])."""
+    points_case("g2_c2_n8192_k1000", 8192, 2, 0, 1e-3, 1000)
+
+
+def long_c2_k200():
+    points_case("g2_c2_n8192_k200", 8192, 2, 0, 1e-3, 200)
+
+
+def long_c3_k200():
+    """C3 (eps=1e-4) at fixed K (parity at K in {200, 1000})."""
+    points_case("g3_c3_n8192_k200", 8192, 2, 0, 1e-4, 200)
+
+
+def long_c3_k1000():
+    points_case("g3_c3_n8192_k1000", 8192, 2, 0, 1e-4, 1000)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")

@@ -100,14 +100,13 @@ def assert_report(rep, z, mu):
     return False
 
 
-@pytest.mark.parametrize("variant", ["stale", "exact", "taskq"])
+@pytest.mark.parametrize("variant", ["stale", "exact"])
 @pytest.mark.parametrize("name", SMALL)
 def test_solve_small(cuda_ok, name, variant):
     z, C64, mu_w, nu_w = fixture_problem(name)
-    stale = variant in ("stale", "taskq")
+    stale = variant == "stale"
     with np.errstate(all="ignore"):
-        rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), config_of(z), stale_shift=stale,
-                             taskq=variant.startswith("taskq"))
+        rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), dist(nu_w), config_of(z), stale_shift=stale)
     if assert_report(rep, z, mu_w) and rep.iterations != int(z["iterations"]):
         # stopped at a different (noise-decided) checkpoint: compare with the
         # oracle run to the same iteration count instead
@@ -117,14 +116,14 @@ def test_solve_small(cuda_ok, name, variant):
         assert_potentials(pot, z)
 
 
-@pytest.mark.parametrize("taskq", [False, True], ids=["fused", "taskq"])
+@pytest.mark.parametrize("mult", [True, False], ids=["mult", "direct"])
 @pytest.mark.parametrize("name", BIG)
-def test_solve_golden_points(cuda_ok, name, taskq):
+def test_solve_golden_points(cuda_ok, name, mult):
     """C1/C2/C3/C5-shaped fixtures; the cost is built on the device (fp64-exact)."""
     z, X, Y, norm = fixture_points(name)
     C = lsk.squared_euclidean_cost(X, Y, normalize=norm)
     assert sha(C.values.cpu().numpy()) == str(z["C32_sha"])  # fp32(C64) bit for bit (SURVEY F5)
-    rep, pot = lsk.solve(C, dist(z["mu"]), dist(z["nu"]), config_of(z), taskq=taskq)
+    rep, pot = lsk.solve(C, dist(z["mu"]), dist(z["nu"]), config_of(z), multiplicative=mult)
     assert_report(rep, z, z["mu"])
     assert_potentials(pot, z)
 

@@ -20,7 +20,6 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-3)
     ap.add_argument("--check", type=int, default=10)
     ap.add_argument("--exact", action="store_true")
-    ap.add_argument("--taskq", action="store_true")
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--general", action="store_true", help="do not pass the uniform-nu flag")
     a = ap.parse_args()
@@ -42,7 +41,7 @@ def main():
     cfg = lsk.SinkhornConfig(epsilon=a.eps, tolerance=1e-30, max_iterations=a.iters, check_interval=a.check)
     ws = None
     for _ in range(a.reps):
-        r, ws = S._launch_solve(torch, C, lm, ln, mu, cfg, stale=not a.exact, ws=ws, taskq=a.taskq,
+        r, ws = S._launch_solve(torch, C, lm, ln, mu, cfg, stale=not a.exact, ws=ws,
                                 uniform_nu=not a.general)
     torch.cuda.synchronize()
     print("iters", r.res.cpu().numpy()[:6], "ms", r.ev0.elapsed_time(r.ev1), flush=True)
