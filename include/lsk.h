@@ -141,6 +141,18 @@ int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t 
                            int32_t normalize_max, float* C, int64_t ldc, double* cmax_out, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* The reference composition without materialising C64 on the host:
+ * lsk_cost_range_f64 -> range_out[0] = max, range_out[1] = min of the fp64
+ * cost (host doubles; CostMatrix.value_range = max - min, types.py:60-86;
+ * synchronises `stream`); lsk_build_cost_div_f32 -> C_ij =
+ * fl32(fl64(sum_k (x_ik - y_jk)^2) / divisor), divisor 0 = none: the fp32 cast
+ * (solver.py:253) of CostMatrix(values=C64 / s) (applications.py:186-188,
+ * estimator.py:87-89) bit for bit. */
+int32_t lsk_cost_range_f64(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, double* range_out,
+                           void* workspace, size_t workspace_bytes, void* stream);
+int32_t lsk_build_cost_div_f32(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, double divisor,
+                               float* C, int64_t ldc, void* stream);
+
 /* dst = fl32(src) in a zero-padded row-major layout (row stride ldd floats,
  * a multiple of 4 for the solver): the one fp64 -> fp32 cast of the cost
  * matrix (solver.py:253), or a plain fp32 re-pad when src_is_f64 == 0. */
@@ -264,6 +276,13 @@ int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int3
 size_t lsk_points_cost_max_workspace_bytes(int32_t B, int32_t n, int32_t m);
 int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
                             double* cmax_out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* range_out (B, 2) device doubles: exact fp64 max and min of the cost per
+ * problem (value_range = max - min, types.py:60-86: the pipelines divide by
+ * C.max() only when it is > 0, applications.py:186-188). */
+size_t lsk_points_cost_range_workspace_bytes(int32_t B, int32_t n, int32_t m);
+int32_t lsk_points_cost_range(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
+                              double* range_out, void* workspace, size_t workspace_bytes, void* stream);
 
 /* NCCL communicator for the sharded points solve (one rank per GPU): rank 0
  * gets an id (lsk_nccl_unique_id_bytes() bytes), every rank passes it to

@@ -55,6 +55,8 @@ SIGNATURES = {
     "lsk_build_cost_workspace_bytes": (_c_sz, []),
     "lsk_build_cost_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p,
                                     _c_sz, _c_p]),
+    "lsk_cost_range_f64": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_build_cost_div_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_dbl, _c_p, _c_i64, _c_p]),
     "lsk_cast_cost_f32": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_p]),
     "lsk_solve_dense_f64_workspace_bytes": (_c_sz, [_c_i32, _c_i32]),
     "lsk_solve_dense_f64": (_c_i32, [_c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_dbl, _c_dbl, _c_i32, _c_i32,
@@ -79,6 +81,8 @@ SIGNATURES = {
     "lsk_points_consume_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_points_consume_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p,
                                         _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_p, _c_sz, _c_p]),
+    "lsk_points_cost_range_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
+    "lsk_points_cost_range": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_points_cost_max_workspace_bytes": (_c_sz, [_c_i32, _c_i32, _c_i32]),
     "lsk_points_cost_max": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_build_cost_f64": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p, _c_sz,

@@ -23,7 +23,7 @@ import numpy as np
 from . import _lib
 from .costs import as_points
 from .errors import DimensionMismatch, NonFiniteResult, ZeroRowMass
-from .points import _batch_points, _weights, points_cost_max, solve_points_otf
+from .points import _batch_points, _weights, points_scale, solve_points_otf
 from .solver import _ptr, _stream_ptr, _torch
 from .types import STATUS_NUMERICAL_FAILURE, SinkhornConfig
 
@@ -75,11 +75,7 @@ def _consume(X, Y, pot, eps, normalize, mu=None, nu=None):
     _, lnu = _weights(nu, B, m, "nu")
     Xd = torch.from_numpy(Xb).to("cuda")
     Yd = torch.from_numpy(Yb).to("cuda")
-    if normalize == "max":
-        cmax = points_cost_max(Xd, Yd)
-        scale = torch.where(cmax > 0, 1.0 / cmax, torch.ones_like(cmax)).to(torch.float32)
-    else:
-        scale = torch.ones(B, dtype=torch.float32, device="cuda")
+    scale = points_scale(Xd, Yd, normalize)  # value_range rule of applications.py:186-188
     f = torch.as_tensor(np.asarray(pot.alpha, np.float32) if not isinstance(pot.alpha, torch.Tensor) else pot.alpha)
     g = torch.as_tensor(np.asarray(pot.beta, np.float32) if not isinstance(pot.beta, torch.Tensor) else pot.beta)
     f = f.to("cuda", torch.float32).reshape(B, n).contiguous()
@@ -116,10 +112,24 @@ def match_point_clouds_with_report(X, Y, eps, config=None):
     if X.shape[1] != Y.shape[1]:
         raise DimensionMismatch(f"point dimensions differ: {X.shape[1]} vs {Y.shape[1]}")
     cfg = config or SinkhornConfig(epsilon=eps)
-    report, pot = solve_points_otf(X, Y, None, None, cfg, normalize="max")
-    if report.status == STATUS_NUMERICAL_FAILURE:
-        raise NonFiniteResult(f"solver reported numerical_failure at eps={eps}")
-    _, idx, wt = _consume(X, Y, pot, cfg.epsilon, "max")
+    if X.shape[1] > 3:  # beyond the on-the-fly kernels (d <= 3): the dense path and its plan
+        from .costs import squared_euclidean_cost
+        from .solver import materialize_plan, solve
+        from .types import make_distribution
+
+        cost = squared_euclidean_cost(X, Y, normalize="max")
+        mu, nu = make_distribution(np.ones(X.shape[0])), make_distribution(np.ones(Y.shape[0]))
+        report, pot = solve(cost, mu, nu, cfg)
+        if report.status == STATUS_NUMERICAL_FAILURE:
+            raise NonFiniteResult(f"solver reported numerical_failure at eps={eps}")
+        P = np.asarray(materialize_plan(cost, mu, nu, pot.alpha, pot.beta, cfg.epsilon).values)
+        idx = P.argmax(axis=1)
+        wt = P[np.arange(P.shape[0]), idx]
+    else:
+        report, pot = solve_points_otf(X, Y, None, None, cfg, normalize="max")
+        if report.status == STATUS_NUMERICAL_FAILURE:
+            raise NonFiniteResult(f"solver reported numerical_failure at eps={eps}")
+        _, idx, wt = _consume(X, Y, pot, cfg.epsilon, "max")
     pairs = [Correspondence(source_index=i, target_index=int(j), weight=float(w))
              for i, (j, w) in enumerate(zip(idx, wt))]
     return pairs, report

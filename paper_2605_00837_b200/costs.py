@@ -1,22 +1,37 @@
 """Cost construction on the device.
 
-``squared_euclidean_cost`` stands in for the reference's
-``costs.squared_euclidean_cost`` (``costs.py:36-50``): the same fp64 direct
-sum over coordinates in coordinate order, computed by ``lsk_build_cost_f32``
-on the GPU and rounded once to the fp32 the solver consumes (solver.py:253),
-so the device matrix equals ``fp32(C64)`` bit for bit. With
-``normalize="max"`` it applies the point-cloud pipeline's ``C / C.max()``
-(``applications.py:186-188``) in fp64 before that rounding.
+``squared_euclidean_cost`` is the reference's ``costs.squared_euclidean_cost``
+(``costs.py:36-50``) with the same return type: a ``CostMatrix`` whose
+``values`` behave as the (n, m) float64 matrix ``sum_k (x_ik - y_jk)^2`` --
+``values.max()`` / ``.min()`` exact, ``value_range`` cached, ``values / s``
+the exact fp64 quotient, ``np.asarray(values)`` the host fp64 matrix -- but
+held as the two point clouds on the device (``SquaredEuclideanValues``). So the
+reference's own composition runs unchanged::
+
+    cost = squared_euclidean_cost(X, Y)
+    if cost.value_range > 0:                                   # applications.py:186-188
+        cost = CostMatrix(values=np.ascontiguousarray(cost.values / cost.values.max()))
+    report, pot = solve(cost, mu, nu, config)
+
+``solve`` on the un-materialised form builds ``fp32(C64 / s)`` directly on the
+device (``lsk_build_cost_div_f32``: the same fp64 direct sum in coordinate
+order, one fp64 division, one fp32 rounding, so bit-identical to the
+reference's cast). ``np.ascontiguousarray`` (as the reference
+pipelines call it) materialises the host fp64 matrix, exactly but at host
+speed; ``normalize="max"`` (or passing ``cost.values / cost.values.max()``
+straight to ``CostMatrix``) keeps it on the device.
 """
+
+import ctypes
 
 import numpy as np
 
 from . import _lib
 from .errors import DimensionMismatch, EmptyInput, NonFiniteInput
 from .solver import _ptr, _stream_ptr, _torch, solve
-from .types import DeviceCostMatrix
+from .types import CostMatrix, DeviceCostMatrix
 
-__all__ = ["as_points", "squared_euclidean_cost", "solve_points"]
+__all__ = ["as_points", "squared_euclidean_cost", "solve_points", "SquaredEuclideanValues"]
 
 
 def as_points(coords):
@@ -33,12 +48,85 @@ def as_points(coords):
     return np.ascontiguousarray(X)
 
 
-def squared_euclidean_cost(X, Y, normalize="none"):
-    """fp32(sum_k (x_ik - y_jk)^2) as a DeviceCostMatrix (see module doc).
+class SquaredEuclideanValues:
+    """fp64-semantics view of ``sum_k (x_ik - y_jk)^2 / s1 / s2 ...`` (never
+    materialised unless converted to a numpy array)."""
 
-    ``normalize``: "none" (reference costs.py) or "max" (divide by the
-    maximum when the range is non-zero, as applications.py:186-188).
-    ``.cmax`` holds the maximum of the un-normalised fp64 cost.
+    __array_priority__ = 1000
+    dtype = np.dtype(np.float64)
+    ndim = 2
+
+    def __init__(self, Xd, Yd, n, m, d, cmax, cmin, divisors=()):
+        self._X, self._Y = Xd, Yd
+        self._n, self._m, self._d = n, m, d
+        self._cmax, self._cmin = float(cmax), float(cmin)
+        self._div = tuple(divisors)
+        self._dev32 = None
+
+    @property
+    def shape(self):
+        return (self._n, self._m)
+
+    @property
+    def size(self):
+        return self._n * self._m
+
+    def _scaled(self, v):
+        for s in self._div:  # Python floats: IEEE fp64 division, as numpy's
+            v = v / s
+        return np.float64(v)
+
+    def max(self):
+        return self._scaled(self._cmax)
+
+    def min(self):
+        return self._scaled(self._cmin)
+
+    def __truediv__(self, s):
+        s = float(s)
+        return SquaredEuclideanValues(self._X, self._Y, self._n, self._m, self._d, self._cmax, self._cmin,
+                                      self._div + (s,))
+
+    def device_f64(self):
+        """The fp64 matrix on the device (n, m), exactly the reference's values."""
+        torch = _torch()
+        C = torch.empty((self._n, self._m), dtype=torch.float64, device="cuda")
+        wsb = _lib.load().lsk_build_cost_workspace_bytes()
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        _lib.call("lsk_build_cost_f64", _ptr(self._X), _ptr(self._Y), self._n, self._m, self._d, 0, _ptr(C),
+                  self._m, None, _ptr(ws), wsb, _stream_ptr(torch))
+        for s in self._div:
+            C = C / s
+        return C
+
+    def __array__(self, dtype=None, copy=None):
+        a = self.device_f64().cpu().numpy()
+        return a if dtype is None else a.astype(dtype)
+
+    def device_fp32(self):
+        """The kernels' padded fp32 layout (cached): fp32(C64 / s) bit for bit."""
+        if self._dev32 is None:
+            torch = _torch()
+            ldc = (self._m + 3) // 4 * 4
+            if len(self._div) <= 1:
+                C = torch.zeros((self._n, ldc), dtype=torch.float32, device="cuda")
+                _lib.call("lsk_build_cost_div_f32", _ptr(self._X), _ptr(self._Y), self._n, self._m, self._d,
+                          self._div[0] if self._div else 0.0, _ptr(C), ldc, _stream_ptr(torch))
+            else:
+                src = self.device_f64()
+                C = torch.empty((self._n, ldc), dtype=torch.float32, device="cuda")
+                _lib.call("lsk_cast_cost_f32", _ptr(src), 1, self._m, self._n, self._m, _ptr(C), ldc,
+                          _stream_ptr(torch))
+            self._dev32 = DeviceCostMatrix(data=C, rows=self._n, cols=self._m, cmax=self._cmax)
+        return self._dev32
+
+
+def squared_euclidean_cost(X, Y, normalize="none"):
+    """``costs.squared_euclidean_cost`` (``costs.py:36-50``) -> ``CostMatrix``
+    with device-held fp64-semantics values (see module doc).
+
+    ``normalize``: "none" (the reference) or "max": divide by the maximum
+    when the range is non-zero, as ``applications.py:186-188``.
     """
     if normalize not in ("none", "max"):
         raise ValueError("normalize must be 'none' or 'max'")
@@ -50,14 +138,14 @@ def squared_euclidean_cost(X, Y, normalize="none"):
     n, m, d = X.shape[0], Y.shape[0], X.shape[1]
     Xd = torch.from_numpy(X).to("cuda")
     Yd = torch.from_numpy(Y).to("cuda")
-    ldc = (m + 3) // 4 * 4
-    C = torch.zeros((n, ldc), dtype=torch.float32, device="cuda")
     wsb = _lib.load().lsk_build_cost_workspace_bytes()
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
-    cmax = torch.zeros(1, dtype=torch.float64, device="cuda")
-    _lib.call("lsk_build_cost_f32", _ptr(Xd), _ptr(Yd), n, m, d, int(normalize == "max"), _ptr(C), ldc,
-              _ptr(cmax), _ptr(ws), wsb, _stream_ptr(torch))
-    return DeviceCostMatrix(data=C, rows=n, cols=m, cmax=float(cmax.item()))
+    rng = (ctypes.c_double * 2)()
+    _lib.call("lsk_cost_range_f64", _ptr(Xd), _ptr(Yd), n, m, d, rng, _ptr(ws), wsb, _stream_ptr(torch))
+    vals = SquaredEuclideanValues(Xd, Yd, n, m, d, rng[0], rng[1])
+    if normalize == "max" and rng[0] - rng[1] > 0:
+        vals = vals / vals.max()
+    return CostMatrix(values=vals, value_range=float(vals.max() - vals.min()))
 
 
 def solve_points(X, Y, mu, nu, config, normalize="none", **kw):

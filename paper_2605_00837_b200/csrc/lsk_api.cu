@@ -416,6 +416,45 @@ int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t 
   return LSK_OK;
 }
 
+// The fp64 max and min of sum_k (x_ik - y_jk)^2 (value_range = max - min,
+// types.py:60-86; the C.max() of applications.py:186-188): range_out[0] = max,
+// range_out[1] = min, host doubles (the call synchronises its stream).
+int32_t lsk_cost_range_f64(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, double* range_out,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  if (!X || !Y || !range_out) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || d < 1) return fail(LSK_EINVAL, "bad shape");
+  if (!workspace || workspace_bytes < lsk_build_cost_workspace_bytes()) return fail(LSK_EINVAL, "workspace too small");
+  cudaStream_t st = S(stream);
+  double* part = static_cast<double*>(workspace);
+  const int blocks = 2048;
+  lsk::k_cost_max<<<blocks, 256, 0, st>>>(X, Y, n, m, d, part);
+  LSK_CUDA(cudaGetLastError());
+  double host[2 * 2048];
+  LSK_CUDA(cudaMemcpyAsync(host, part, sizeof(host), cudaMemcpyDeviceToHost, st));
+  LSK_CUDA(cudaStreamSynchronize(st));
+  double mx = -1.0, mn = INFINITY;
+  for (int k = 0; k < blocks; ++k) {
+    mx = host[2 * k] > mx ? host[2 * k] : mx;
+    mn = host[2 * k + 1] < mn ? host[2 * k + 1] : mn;
+  }
+  range_out[0] = mx;
+  range_out[1] = mn;
+  return LSK_OK;
+}
+
+// C_ij = fl32(fl64(sum_k (x_ik - y_jk)^2) / divisor) (divisor 0: no division):
+// the reference's CostMatrix(values=C64 / s) rounded once to fp32 (solver.py:253).
+int32_t lsk_build_cost_div_f32(const double* X, const double* Y, int32_t n, int32_t m, int32_t d, double divisor,
+                               float* C, int64_t ldc, void* stream) {
+  if (!X || !Y || !C) return fail(LSK_EINVAL, "null pointer");
+  if (n < 1 || m < 1 || d < 1 || ldc < m) return fail(LSK_EINVAL, "bad shape");
+  int bx = (m + 255) / 256;
+  if (bx > 64) bx = 64;
+  lsk::k_cost_build<<<dim3(bx, n < 65535 ? n : 65535), 256, 0, S(stream)>>>(X, Y, n, m, d, divisor, C, ldc);
+  LSK_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
 int32_t lsk_cast_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int32_t n, int32_t m, float* dst,
                           int64_t ldd, void* stream) {
   if (!src || !dst) return fail(LSK_EINVAL, "null pointer");

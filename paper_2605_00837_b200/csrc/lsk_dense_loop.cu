@@ -3,8 +3,10 @@
 // decision on the device (no host synchronisation inside the loop).
 //
 // Reference path replaced: solve (solver.py:230-337) exactly as the reference
-// orders it: per iteration the alpha step (76-80) as a two-pass row LSE
-// (k_row_lse<kRowAlpha>), the beta step (83-94) as coalesced column (max,
+// orders it: per iteration the alpha step (76-80) as a row LSE -- one pass
+// shifted by the previous f with an exact two-pass fallback per row
+// (k_row_alpha_stale, LSK_FLAG_STALE_SHIFT) or the exact two-pass
+// k_row_lse<kRowAlpha> -- the beta step (83-94) as coalesced column (max,
 // sumexp) partials + fixed-order combine (k_col_pairs / k_col_combine), and at
 // every checkpoint the finiteness test and the reference marginal-error formula
 // (97-104, k_row_lse<kRowCheck>) summed in fixed 1024-row blocks; the extra
@@ -17,6 +19,7 @@
 #include "../../include/lsk.h"
 #include "lsk_kernels.cuh"
 #include "lsk_points.cuh"
+#include "lsk_poll.h"
 
 namespace lsk_host {
 int32_t fail(int32_t code, const std::string& msg);
@@ -136,9 +139,17 @@ int32_t solve_dense_loop(const float* C, int64_t ldc, int32_t n, int32_t m, cons
     return LSK_OK;
   };
   int32_t rc;
+  const bool stale = (flags & LSK_FLAG_STALE_SHIFT) != 0;
+  lsk_poll::StopPoll poll;
+  if ((rc = poll.init(1, st))) return rc;
   for (int k = 1; k <= K; ++k) {
-    if (k > 1 && (k - 1) % c == 0 && (rc = check(k - 1, false))) return rc;
-    if (k > 1)  // one read of the row, shifted by the stale f (exact fallback per row)
+    if (k > 1 && (k - 1) % c == 0) {
+      if ((rc = check(k - 1, false))) return rc;
+      bool stop = false;
+      if ((rc = poll.after_check(act, st, stop))) return rc;
+      if (stop) break;
+    }
+    if (k > 1 && stale)  // one read of the row, shifted by the stale f (exact fallback per row)
       lsk::k_row_alpha_stale<<<n, 256, 0, st>>>(C, ldc, n, m, F[(k - 1) & 1], G[(k - 1) & 1], log_nu, inv_eps, neg_eps,
                                                 F[k & 1], act);
     else

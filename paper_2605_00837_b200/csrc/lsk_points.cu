@@ -33,6 +33,15 @@ int32_t pfail(int32_t code, const std::string& msg) { return lsk_host::fail(code
 inline size_t al(size_t x) { return (x + 255) / 256 * 256; }
 inline int chunks_of(int ncols) { return (ncols + lsk::kPtsChunk - 1) / lsk::kPtsChunk; }
 
+__global__ void k_fill_u64(unsigned long long* p, int count, unsigned long long v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) p[i] = v;
+}
+__global__ void k_interleave2(const double* a, const double* b, int count, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) { out[2 * i] = a[i]; out[2 * i + 1] = b[i]; }
+}
+
 struct EpsC {
   float inv, neg;
 };
@@ -151,4 +160,34 @@ extern "C" int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t
   lsk::k_pts_cmax2<1><<<grid, lsk::kPtsThreads, 0, st>>>(n, m, d, X4, Y4, X, Y, m32, m64);
   P_CUDA(cudaGetLastError());
   return LSK_OK;
+}
+
+// (B, 2) device doubles: [b][0] = exact fp64 max, [b][1] = exact fp64 min of
+// sum_k (x_ik - y_jk)^2 -- the max/min behind CostMatrix.value_range
+// (types.py:60-86) for the pipelines' C / C.max() gate (applications.py:186).
+extern "C" int32_t lsk_points_cost_range(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
+                                         double* range_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!range_out) return pfail(LSK_EINVAL, "null pointer");
+  if (!workspace || workspace_bytes < lsk_points_cost_max_workspace_bytes(B, n, m) + al(size_t(B) * 16))
+    return pfail(LSK_EINVAL, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = static_cast<char*>(workspace);
+  const size_t base = lsk_points_cost_max_workspace_bytes(B, n, m);
+  double* mx = reinterpret_cast<double*>(ws + base);
+  double* mn = mx + B;
+  int32_t rc = lsk_points_cost_max(X, Y, B, n, m, d, mx, workspace, base, stream);
+  if (rc != LSK_OK) return rc;
+  const unsigned long long inf_bits = 0x7FF0000000000000ull;
+  P_CUDA(cudaMemsetAsync(mn, 0, size_t(B) * 8, st));
+  k_fill_u64<<<(B + 127) / 128, 128, 0, st>>>(reinterpret_cast<unsigned long long*>(mn), B, inf_bits);
+  lsk::k_pts_cmin64<<<dim3((m + 255) / 256, (n + 63) / 64, B), 256, 0, st>>>(
+      n, m, d, X, Y, reinterpret_cast<unsigned long long*>(mn));
+  k_interleave2<<<(B + 127) / 128, 128, 0, st>>>(mx, mn, B, range_out);
+  P_CUDA(cudaGetLastError());
+  return LSK_OK;
+}
+
+extern "C" size_t lsk_points_cost_range_workspace_bytes(int32_t B, int32_t n, int32_t m) {
+  if (B < 1 || n < 1 || m < 1) return 0;
+  return lsk_points_cost_max_workspace_bytes(B, n, m) + al(size_t(B) * 16);
 }

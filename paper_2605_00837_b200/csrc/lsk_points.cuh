@@ -719,4 +719,34 @@ static __global__ void __launch_bounds__(kPtsThreads) k_pts_cmax2(int n, int m, 
   }
 }
 
+
+// Exact fp64 min of the direct coordinate sum (costs.py:48-49) per problem:
+// value_range = max - min decides the C / C.max() of applications.py:186-188.
+// One thread per column j, 64 rows per CTA (row loads are warp-uniform).
+static __global__ void __launch_bounds__(256) k_pts_cmin64(int n, int m, int d, const double* __restrict__ X,
+                                                          const double* __restrict__ Y,
+                                                          unsigned long long* __restrict__ min64) {
+  const int b = blockIdx.z;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i0 = blockIdx.y * 64;
+  double y[3] = {0.0, 0.0, 0.0};
+  if (j < m)
+    for (int k = 0; k < d; ++k) y[k] = Y[((size_t)b * m + j) * d + k];
+  double mn = INFINITY;
+  const int i1 = min(n, i0 + 64);
+  for (int i = i0; i < i1; ++i) {
+    const double* xp = X + ((size_t)b * n + i) * d;
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double t = __dsub_rn(xp[k], y[k]);
+      acc = (k == 0) ? __dmul_rn(t, t) : __dadd_rn(acc, __dmul_rn(t, t));
+    }
+    mn = fmin(mn, acc);
+  }
+  if (j >= m) mn = INFINITY;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(min64 + b, static_cast<unsigned long long>(__double_as_longlong(mn)));
+}
+
 }  // namespace lsk

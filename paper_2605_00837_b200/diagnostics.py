@@ -14,6 +14,8 @@ __all__ = ["kkt_residual", "regularized_objective", "contraction_rate_bound"]
 
 
 def _dev(torch, a, dt):
+    if hasattr(a, "device_f64"):  # costs.SquaredEuclideanValues
+        return a.device_f64().to(dt)
     if isinstance(a, torch.Tensor):
         return a.to("cuda", dt).contiguous()
     return torch.from_numpy(np.ascontiguousarray(np.asarray(a))).to("cuda", dt)

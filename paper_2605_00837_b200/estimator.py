@@ -72,11 +72,14 @@ class SinkhornTransport(TransformerMixin, BaseEstimator):
         if report.status == STATUS_NUMERICAL_FAILURE:
             raise NonFiniteResult(f"transport solve failed numerically at epsilon={self.epsilon}")
         plan = solver64.materialize_plan(C, mu, nu, pot.alpha, pot.beta, self.epsilon, return_device=True)
-        if d > 4:
-            raise ValueError("the B200 estimator maps points of dimension 1..4")
         mapped = torch.empty((n, d), dtype=torch.float64, device="cuda")
         flags = torch.zeros(2, dtype=torch.int32, device="cuda")
-        _lib.call("lsk_barycentric_plan_f64", _ptr(plan.values), m, n, m, _ptr(Yd), d, _ptr(mapped), _ptr(flags), st)
+        for k0 in range(0, d, 4):  # the barycentric kernel maps up to 4 coordinates per pass
+            dt = min(4, d - k0)
+            Yk = Yd[:, k0:k0 + dt].contiguous()
+            mk = torch.empty((n, dt), dtype=torch.float64, device="cuda")
+            _lib.call("lsk_barycentric_plan_f64", _ptr(plan.values), m, n, m, _ptr(Yk), dt, _ptr(mk), _ptr(flags), st)
+            mapped[:, k0:k0 + dt] = mk
         if int(flags[1].item()):
             raise ZeroRowMass("a transport plan row has zero total mass")
         self.source_ = X

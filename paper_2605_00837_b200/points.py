@@ -11,15 +11,18 @@ registers. Returns the reference's ``(SolveReport, DualPotentials)``.
   is sharded over the ranks: ``shard="partials"`` (default: row
   slabs of the source cloud, per-column partials exchanged and merged by a
   fixed tree), ``"allreduce"`` (stale sums by ncclAllReduce) or ``"owner"``
-  (owner computes, potential slabs allgathered). ``emulate_ranks=P`` runs the
-  same P-rank decomposition on one GPU (collectives as device copies) and
-  checks that every virtual rank ends bit-identical.
+  (owner computes, potential slabs allgathered).
+* ``solve_points_emulated``: the same P-rank decomposition on one GPU
+  (collectives as device copies); reports whether every virtual rank ended
+  bit-identical.
 * ``solve_points_batched``: B independent problems of one shape in a single
   launch sequence; each problem stops on its own (per-problem status / trace).
 
 Numerics: fp32 cost from fp32-rounded points in the direct form (SURVEY F5:
-~2-3e-6 on the potentials at eps=1e-3). ``costs.solve_points`` picks this path
-automatically only where the fp64-exact dense matrix does not fit (m > 8192).
+~2-3e-6 on the potentials at eps=1e-3). Callers choose the path:
+``costs.solve_points`` always builds the fp64-exact dense matrix (bit-identical
+to the reference's cast); this module is the on-the-fly path for clouds whose
+(n, m) matrix should not be stored (C4: 17 GB) and for batches (C5).
 """
 
 import time
@@ -62,6 +65,29 @@ def _weights(dist, B, k, name):
     if w.shape != (B, k):
         raise DimensionMismatch(f"{name}: weights of shape {w.shape}, expected {(B, k)}")
     return w, lw
+
+
+def points_cost_range(Xd, Yd):
+    """(B, 2) device doubles: the exact fp64 max and min of the cost per problem."""
+    torch = _torch()
+    B, n, d = Xd.shape
+    m = Yd.shape[1]
+    out = torch.empty((B, 2), dtype=torch.float64, device="cuda")
+    wsb = _lib.load().lsk_points_cost_range_workspace_bytes(B, n, m)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.call("lsk_points_cost_range", _ptr(Xd), _ptr(Yd), B, n, m, d, _ptr(out), _ptr(ws), wsb, _stream_ptr(torch))
+    return out
+
+
+def points_scale(Xd, Yd, normalize):
+    """(B,) fp32 cost scale: 1/C.max() where value_range > 0 (applications.py:186-188), else 1."""
+    torch = _torch()
+    B = Xd.shape[0]
+    if normalize != "max":
+        return torch.ones(B, dtype=torch.float32, device="cuda")
+    r = points_cost_range(Xd, Yd)
+    cmax, cmin = r[:, 0], r[:, 1]
+    return torch.where(cmax > cmin, 1.0 / cmax, torch.ones_like(cmax)).to(torch.float32)
 
 
 def points_cost_max(Xd, Yd):
@@ -107,7 +133,8 @@ def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=F
             emulate_ranks=None):
     torch = _torch()
     if config.precision != "single":
-        raise NotImplementedError("precision='double' is not available on the B200 path (fp32 only)")
+        raise NotImplementedError("the on-the-fly points solver computes in fp32; use precision='single', or "
+                                  "solve(squared_euclidean_cost(X, Y), ...) for precision='double'")
     if normalize not in ("none", "max"):
         raise ValueError("normalize must be 'none' or 'max'")
     Xb, Yb = _batch_points(X), _batch_points(Y)
@@ -122,12 +149,8 @@ def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=F
     r.B, r.n, r.m = B, n, m
     Xd = torch.from_numpy(Xb).to("cuda")
     Yd = torch.from_numpy(Yb).to("cuda")
-    if normalize == "max":
-        cmax = points_cost_max(Xd, Yd)
-        # reference: C / C.max() only when the cost has a non-zero range (applications.py:186-188)
-        scale = torch.where(cmax > 0, 1.0 / cmax, torch.ones_like(cmax)).to(torch.float32)
-    else:
-        scale = torch.ones(B, dtype=torch.float32, device="cuda")
+    # reference: C / C.max() only when the cost has a non-zero range (applications.py:186-188)
+    scale = points_scale(Xd, Yd, normalize)
     lmu_d = torch.from_numpy(lmu.astype(np.float32)).to("cuda")
     lnu_d = torch.from_numpy(lnu.astype(np.float32)).to("cuda")
     mu_d = torch.from_numpy(wmu.astype(np.float32)).to("cuda")

@@ -8,10 +8,11 @@ solver.py:46-57``): ``solve`` (230-337), ``update_alpha`` (118-140),
 one C-ABI call of ``liblsk.so`` (include/lsk.h); all arithmetic runs in the
 sm_100a kernels. Device memory and streams come from PyTorch.
 
-Precision: the B200 path computes in fp32 (``precision="single"``), which is
-the reference's default and the parity target. ``precision="double"`` and
-float64 potentials raise ``NotImplementedError`` rather than silently
-computing in a different precision.
+Precision: ``precision="single"`` (the reference's default and the parity
+target) runs the fp32 kernels; ``precision="double"`` and float64 potentials
+in the half-steps follow the reference's dtype rule (``solver.py:60-65``) and
+run the fp64 kernels (``solver64``, ``lsk_*_f64``) with the reference's double
+arithmetic -- never a silent change of precision.
 """
 
 import time
@@ -84,6 +85,8 @@ def to_device_cost(cost):
     if isinstance(cost, DeviceCostMatrix):
         return cost
     vals = cost.values if isinstance(cost, CostMatrix) else cost
+    if hasattr(vals, "device_fp32"):  # costs.SquaredEuclideanValues: built on the device, never materialised
+        return vals.device_fp32()
     if isinstance(vals, np.ndarray):
         if vals.ndim != 2:
             raise DimensionMismatch("cost matrix must be 2-D")
@@ -135,6 +138,7 @@ def _uniform(log_w):
 
 def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None,
                   uniform_nu=False, mult=True):
+    C = to_device_cost(C)
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
     cap = _lib.load().lsk_trace_capacity(K, c)

@@ -38,6 +38,8 @@ def float_dtype(*arrays):
 
 def _cost64(torch, cost):
     vals = cost.values if isinstance(cost, CostMatrix) else getattr(cost, "data", cost)
+    if hasattr(vals, "device_f64"):  # costs.SquaredEuclideanValues
+        return vals.device_f64()
     if isinstance(vals, torch.Tensor):
         t = vals.to("cuda", torch.float64)
         if hasattr(cost, "cols") and t.shape[1] != cost.cols:  # DeviceCostMatrix padding

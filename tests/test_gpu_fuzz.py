@@ -11,6 +11,7 @@ import pytest
 
 import lsk_oracle as O
 import paper_2605_00837_b200 as lsk
+from conftest import rel_max_floor
 
 pytestmark = pytest.mark.gpu
 
@@ -46,9 +47,8 @@ def test_random_problem_vs_oracle(cuda_ok, seed):
     assert rep.status == ref["status"] and rep.iterations == ref["iterations"], (seed, rep.status, ref["status"])
     if ref["status"] == "numerical_failure":
         return
-    scale = max(np.abs(ref["alpha"]).max(), np.abs(ref["beta"]).max())
-    ea = np.abs(pot.alpha - ref["alpha"]).max() / scale
-    eb = np.abs(pot.beta - ref["beta"]).max() / scale
+    ea = rel_max_floor(pot.alpha, ref["alpha"], ref["beta"])
+    eb = rel_max_floor(pot.beta, ref["beta"], ref["alpha"])
     assert ea <= 1e-5 and eb <= 1e-5, (seed, n, m, eps, K, ea, eb)
     assert abs(rep.transport_cost - ref["cost"]) <= 1e-5 * abs(ref["cost"]) + 1e-7
     assert [k for k, _ in rep.error_trace] == [k for k, _ in ref["trace"]]
@@ -72,7 +72,6 @@ def test_wide_m_loop_vs_oracle(cuda_ok, seed):
     with np.errstate(all="ignore"):
         ref = O.solve(C64, mu.weights, nu.weights, eps, tol=1e-30, max_iter=K, check=c)
     assert rep.status == ref["status"] and rep.iterations == ref["iterations"]
-    scale = max(np.abs(ref["alpha"]).max(), np.abs(ref["beta"]).max())
-    assert np.abs(pot.alpha - ref["alpha"]).max() <= 1e-5 * scale
-    assert np.abs(pot.beta - ref["beta"]).max() <= 1e-5 * scale
+    assert rel_max_floor(pot.alpha, ref["alpha"], ref["beta"]) <= 1e-5
+    assert rel_max_floor(pot.beta, ref["beta"], ref["alpha"]) <= 1e-5
     assert abs(rep.transport_cost - ref["cost"]) <= 1e-5 * abs(ref["cost"]) + 1e-7

@@ -13,6 +13,7 @@ import pytest
 
 import lsk_oracle as O
 import paper_2605_00837_b200 as lsk
+from paper_2605_00837_b200.solver import to_device_cost
 from conftest import golden, golden_names, rel_max, sha
 from inputs import fixture_points, fixture_problem
 
@@ -122,7 +123,7 @@ def test_solve_golden_points(cuda_ok, name, mult):
     """C1/C2/C3/C5-shaped fixtures; the cost is built on the device (fp64-exact)."""
     z, X, Y, norm = fixture_points(name)
     C = lsk.squared_euclidean_cost(X, Y, normalize=norm)
-    assert sha(C.values.cpu().numpy()) == str(z["C32_sha"])  # fp32(C64) bit for bit (SURVEY F5)
+    assert sha(to_device_cost(C).values.cpu().numpy()) == str(z["C32_sha"])  # fp32(C64) bit for bit (SURVEY F5)
     rep, pot = lsk.solve(C, dist(z["mu"]), dist(z["nu"]), config_of(z), multiplicative=mult)
     assert_report(rep, z, z["mu"])
     assert_potentials(pot, z)

@@ -20,6 +20,7 @@ import pytest
 
 import lsk_oracle as O
 import paper_2605_00837_b200 as lsk
+from paper_2605_00837_b200.solver import to_device_cost
 from conftest import GOLDEN, golden, rel_max, sha
 from inputs import fixture_points
 from paper_2605_00837_b200 import points as PT
@@ -76,7 +77,7 @@ def test_dense_benchmarked_configs(cuda_ok, name, mult):
         pytest.skip(f"fixture {name} not generated")
     z, X, Y, norm = fixture_points(name)
     C = lsk.squared_euclidean_cost(X, Y)
-    assert sha(C.values.cpu().numpy()) == str(z["C32_sha"])
+    assert sha(to_device_cost(C).values.cpu().numpy()) == str(z["C32_sha"])
     rep, pot = lsk.solve(C, dist(z["mu"]), dist(z["nu"]), config_of(z), multiplicative=mult)
     check(name, "mult" if mult else "direct", rep, pot, z)
 

@@ -13,6 +13,7 @@ import pytest
 import lsk_oracle as O
 import paper_2605_00837_b200 as lsk
 
+from conftest import rel_max_floor
 from inputs import fixture_points
 from paper_2605_00837_b200 import points as PT
 
@@ -43,9 +44,8 @@ def test_points_fixture(cuda_ok, name, variant):
     # marginal errors: same trajectory within fp32-cost noise
     for (_, e), (_, er) in zip(rep.error_trace, z["trace"]):
         assert abs(e - er) <= 2e-3 * abs(er) + 2e-6, (e, er)
-    scale = max(np.abs(z["alpha"]).max(), np.abs(z["beta"]).max())
-    assert np.abs(pot.alpha - z["alpha"]).max() <= RTOL * scale
-    assert np.abs(pot.beta - z["beta"]).max() <= RTOL * scale
+    assert rel_max_floor(pot.alpha, z["alpha"], z["beta"]) <= RTOL
+    assert rel_max_floor(pot.beta, z["beta"], z["alpha"]) <= RTOL
     assert abs(rep.transport_cost - float(z["cost"])) <= RTOL * abs(float(z["cost"]))
 
 
@@ -94,9 +94,8 @@ def test_points_vs_oracle_ragged(cuda_ok):
         ref = O.solve(C64, mu_w, nu_w, eps, tol=1e-30, max_iter=K, check=10)
         rep, pot = PT.solve_points_otf(X, Y, None, None,
                                        lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=K))
-        scale = max(np.abs(ref["alpha"]).max(), np.abs(ref["beta"]).max())
-        assert np.abs(pot.alpha - ref["alpha"]).max() <= RTOL * scale, (n, m, d)
-        assert np.abs(pot.beta - ref["beta"]).max() <= RTOL * scale, (n, m, d)
+        assert rel_max_floor(pot.alpha, ref["alpha"], ref["beta"]) <= RTOL, (n, m, d)
+        assert rel_max_floor(pot.beta, ref["beta"], ref["alpha"]) <= RTOL, (n, m, d)
         assert abs(rep.transport_cost - ref["cost"]) <= RTOL * abs(ref["cost"])
 
 
@@ -143,6 +142,5 @@ def test_points_guard_path_matches_online(cuda_ok):
     cfg = lsk.SinkhornConfig(epsilon=3e-4, tolerance=1e-30, max_iterations=15)
     r1, p1 = PT.solve_points_otf(X * 3, Y * 3, None, None, cfg, stale_shift=True)
     r2, p2 = PT.solve_points_otf(X * 3, Y * 3, None, None, cfg, stale_shift=False)
-    scale = max(np.abs(p2.alpha).max(), np.abs(p2.beta).max())
-    assert np.abs(p1.alpha - p2.alpha).max() <= 1e-5 * scale
-    assert np.abs(p1.beta - p2.beta).max() <= 1e-5 * scale
+    assert rel_max_floor(p1.alpha, p2.alpha, p2.beta) <= 1e-5
+    assert rel_max_floor(p1.beta, p2.beta, p2.alpha) <= 1e-5
