@@ -96,7 +96,9 @@ class SquaredEuclideanValues:
         _lib.call("lsk_build_cost_f64", _ptr(self._X), _ptr(self._Y), self._n, self._m, self._d, 0, _ptr(C),
                   self._m, None, _ptr(ws), wsb, _stream_ptr(torch))
         for s in self._div:
-            C = C / s
+            # a device tensor divisor: an IEEE division per element (torch turns a
+            # Python-scalar divisor into a multiplication by its reciprocal)
+            C = torch.div(C, torch.full((1, 1), s, dtype=torch.float64, device="cuda"))
         return C
 
     def __array__(self, dtype=None, copy=None):

@@ -84,7 +84,8 @@ int32_t lsk_comm_destroy(void* comm) {
 size_t lsk_points_consume_workspace_bytes(int32_t B, int32_t n, int32_t m) {
   if (B < 1 || n < 1 || m < 1) return 0;
   const size_t ch = size_t(chunks_of(m));
-  return al(size_t(B) * n * 16) + al(size_t(B) * m * 16) + al(size_t(B) * ch * n * 16) + al(size_t(B) * ch * n * 8);
+  return al(size_t(B) * n * 16) + al(size_t(B) * m * 16) + al(size_t(B) * ch * n * 16) + al(size_t(B) * ch * n * 8) +
+         al(size_t(B) * 24);
 }
 
 int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
@@ -109,15 +110,18 @@ int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int3
   float4* part = reinterpret_cast<float4*>(ws);
   ws += al(size_t(B) * chunks * n * 16);
   float2* best = reinterpret_cast<float2*>(ws);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, X, n, X4);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, X, n, Y4);
+  ws += al(size_t(B) * chunks * n * 8);
+  double* ctr = reinterpret_cast<double*>(ws);
+  lsk::k_pts_center<<<B, 256, 0, st>>>(X, Y, n, m, d, ctr);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, ctr, X4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, ctr, Y4);
   const EpsC ec = epsc(eps);
   lsk::PtsConsume h{B, n, m, chunks, X4, Y4, f, g, log_nu, scale, ec.inv, part, best};
   const int tiles = (n + lsk::kPtsTileRows - 1) / lsk::kPtsTileRows;
   lsk::k_pts_consume<<<dim3(chunks, tiles, B), lsk::kPtsThreads, 0, st>>>(h);
   lsk::k_pts_consume_finish<<<dim3((n + 255) / 256, B), 256, 0, st>>>(B, n, m, d, chunks, part, best, X4, Y4, f, g,
                                                                     log_mu, log_nu, scale, ec.inv, mapped_out,
-                                                                    match_idx, match_w, zero_rows, X);
+                                                                    match_idx, match_w, zero_rows, ctr);
   P_CUDA(cudaGetLastError());
   return LSK_OK;
 }
@@ -128,12 +132,13 @@ int32_t lsk_points_consume_f32(const double* X, const double* Y, int32_t B, int3
 // applications.py:186-188) without materialising C: an fp32 screen of all
 // pairs on translated points, then exact fp64 re-evaluation of the pairs within
 // 1e-5 of the screened max. The fp32 value of any pair is within ~1e-6
-// relative of its exact value (translation by a data point bounds the rounded
-// coordinates by twice the largest pair distance), so the true maximiser is
-// always among the re-evaluated pairs.
+// relative of its exact value (translation to the bounding-box centre bounds
+// the rounded coordinates by the box half-diagonal, at most sqrt(3)/2 of the
+// largest pair distance's span), so the true maximiser is always among the
+// re-evaluated pairs.
 extern "C" size_t lsk_points_cost_max_workspace_bytes(int32_t B, int32_t n, int32_t m) {
   if (B < 1 || n < 1 || m < 1) return 0;
-  return al(size_t(B) * n * 16) + al(size_t(B) * m * 16) + al(size_t(B) * 4);
+  return al(size_t(B) * n * 16) + al(size_t(B) * m * 16) + al(size_t(B) * 4) + al(size_t(B) * 24);
 }
 
 extern "C" int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t B, int32_t n, int32_t m, int32_t d,
@@ -150,8 +155,11 @@ extern "C" int32_t lsk_points_cost_max(const double* X, const double* Y, int32_t
   float4* Y4 = reinterpret_cast<float4*>(ws);
   ws += al(size_t(B) * m * 16);
   unsigned* m32 = reinterpret_cast<unsigned*>(ws);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, X, n, X4);
-  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, X, n, Y4);
+  ws += al(size_t(B) * 4);
+  double* ctr = reinterpret_cast<double*>(ws);
+  lsk::k_pts_center<<<B, 256, 0, st>>>(X, Y, n, m, d, ctr);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(X, (long long)B * n, n, d, ctr, X4);
+  lsk::k_pts_pack<<<256, 256, 0, st>>>(Y, (long long)B * m, m, d, ctr, Y4);
   P_CUDA(cudaMemsetAsync(m32, 0, size_t(B) * 4, st));
   P_CUDA(cudaMemsetAsync(cmax_out, 0, size_t(B) * 8, st));
   const dim3 grid(chunks_of(m), (n + lsk::kPtsTileRows - 1) / lsk::kPtsTileRows, B);

@@ -453,16 +453,48 @@ static __global__ void k_pts_cost_finish(int B, int n, const float* __restrict__
   s.cost = c;
 }
 
+// Per problem, the centre of the bounding box of both clouds (fp64; ctr is
+// (B, 3), unused coordinates 0): the translation of k_pts_pack.
+static __global__ void __launch_bounds__(256) k_pts_center(const double* __restrict__ X, const double* __restrict__ Y,
+                                                          int n, int m, int d, double* __restrict__ ctr) {
+  __shared__ double smn[3][8], smx[3][8];
+  const int b = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < 3; ++k) {
+    double mn = INFINITY, mx = -INFINITY;
+    if (k < d) {
+      for (int i = threadIdx.x; i < n + m; i += blockDim.x) {
+        const double v = i < n ? X[((size_t)b * n + i) * d + k] : Y[((size_t)b * m + (i - n)) * d + k];
+        mn = fmin(mn, v);
+        mx = fmax(mx, v);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) { smn[k][w] = mn; smx[k][w] = mx; }
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    const int k = threadIdx.x;
+    double mn = INFINITY, mx = -INFINITY;
+    for (int q = 0; q < 8; ++q) { mn = fmin(mn, smn[k][q]); mx = fmax(mx, smx[k][q]); }
+    ctr[b * 3 + k] = (k < d) ? __dmul_rn(__dadd_rn(mn, mx), 0.5) : 0.0;
+  }
+}
+
 // fp64 points -> float4 (x, y, z, 0), coordinates beyond d zero. Each problem
-// is translated by its first source point x_b0 in fp64 before the single fp32
-// rounding: distances are unchanged, and the fp32 coordinates carry the data's
-// spread instead of its offset (the on-the-fly cost stays accurate for clouds
-// far from the origin).
+// is translated by the centre of its bounding box (k_pts_center) in fp64
+// before the single fp32 rounding: distances are unchanged, and the fp32
+// coordinates carry the data's spread (|x - c| <= half the box diagonal)
+// instead of its offset, which keeps the on-the-fly cost accurate for clouds
+// far from the origin and halves the expansion form's cancellation.
 static __global__ void k_pts_pack(const double* __restrict__ P, long long count, int per_problem, int d,
-                                  const double* __restrict__ X, int n, float4* __restrict__ out) {
+                                  const double* __restrict__ ctr, float4* __restrict__ out) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
     const long long b = i / per_problem;
-    const double* c = X + b * (long long)n * d;
+    const double* c = ctr + b * 3;
     float v[3] = {0.f, 0.f, 0.f};
     for (int k = 0; k < d; ++k) v[k] = __double2float_rn(__dsub_rn(P[i * d + k], c[k]));
     out[i] = make_float4(v[0], v[1], v[2], 0.f);
@@ -579,7 +611,7 @@ static __global__ void k_pts_consume_finish(int B, int n, int m, int d, int chun
                                             const float* __restrict__ lnu, const float* __restrict__ scale,
                                             float inv_eps, float* __restrict__ mapped, int* __restrict__ idx,
                                             float* __restrict__ wt, int* __restrict__ zero_rows,
-                                            const double* __restrict__ X0) {
+                                            const double* __restrict__ ctr) {
   const int b = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -595,8 +627,8 @@ static __global__ void k_pts_consume_finish(int B, int n, int m, int d, int chun
   }
   const size_t ri = (size_t)b * n + i;
   if (!(a0 > 0.f)) atomicAdd(zero_rows, 1);  // ZeroRowMass (applications.py:92-93)
-  // undo the translation of k_pts_pack (points were shifted by the problem's first source point)
-  const double* c0 = X0 + (size_t)b * n * d;
+  // undo the translation of k_pts_pack (points were shifted by the problem's box centre)
+  const double* c0 = ctr + (size_t)b * 3;
   const float out[3] = {a1 / a0, a2 / a0, a3 / a0};
   for (int k = 0; k < d; ++k) mapped[ri * d + k] = __double2float_rn(__dadd_rn(double(out[k]), c0[k]));
   if (j == 0x7fffffff) j = 0;

@@ -118,7 +118,7 @@ int32_t make_shard(int n, int m, int P, int mode, Shard& s) {
 }
 
 struct PtsLayout {
-  size_t x4, y4, f0, f1, g0, g1, fsel, gsel, part, slots, rowflag, nflag, errrow, errblk, bad, badslots, costrow, costblk, state,
+  size_t x4, y4, ctr, f0, f1, g0, g1, fsel, gsel, part, slots, rowflag, nflag, errrow, errblk, bad, badslots, costrow, costblk, state,
       act, total;
 };
 
@@ -131,6 +131,7 @@ PtsLayout pts_layout(int B, int n, int m, const Shard& s) {
   const int nb = (s.npad + lsk::kPtsBlk - 1) / lsk::kPtsBlk;
   L.x4 = o; o = al(o + size_t(B) * n * 16);
   L.y4 = o; o = al(o + size_t(B) * m * 16);
+  L.ctr = o; o = al(o + size_t(B) * 24);
   L.f0 = o; o = al(o + size_t(B) * s.npad * 4);
   L.f1 = o; o = al(o + size_t(B) * s.npad * 4);
   L.g0 = o; o = al(o + size_t(B) * s.mpad * 4);
@@ -235,6 +236,7 @@ struct Rank {
   int r = 0;
   char* base = nullptr;
   float4 *X4, *Y4;
+  double* ctr;
   float *F[2], *G[2];
   float *fsel, *gsel;  // the returned iterate
   void *part, *slots;
@@ -253,6 +255,7 @@ void carve(Rank& R, char* ws, const PtsLayout& L) {
   R.base = ws;
   R.X4 = reinterpret_cast<float4*>(ws + L.x4);
   R.Y4 = reinterpret_cast<float4*>(ws + L.y4);
+  R.ctr = reinterpret_cast<double*>(ws + L.ctr);
   R.F[0] = reinterpret_cast<float*>(ws + L.f0);
   R.F[1] = reinterpret_cast<float*>(ws + L.f1);
   R.G[0] = reinterpret_cast<float*>(ws + L.g0);
@@ -361,8 +364,9 @@ int32_t run_solve(const SolveArgs& a, const Shard& sh, std::vector<Rank>& ranks,
     S_CUDA(cudaMemsetAsync(R.bad, 0, size_t(B) * 4, st));
     S_CUDA(cudaMemsetAsync(R.errrow, 0, size_t(B) * sh.npad * 4, st));
     S_CUDA(cudaMemsetAsync(R.costrow, 0, size_t(B) * sh.npad * 4, st));
-    lsk::k_pts_pack<<<256, 256, 0, st>>>(a.X, (long long)B * n, n, a.d, a.X, n, R.X4);
-    lsk::k_pts_pack<<<256, 256, 0, st>>>(a.Y, (long long)B * m, m, a.d, a.X, n, R.Y4);
+    lsk::k_pts_center<<<B, 256, 0, st>>>(a.X, a.Y, n, m, a.d, R.ctr);
+    lsk::k_pts_pack<<<256, 256, 0, st>>>(a.X, (long long)B * n, n, a.d, R.ctr, R.X4);
+    lsk::k_pts_pack<<<256, 256, 0, st>>>(a.Y, (long long)B * m, m, a.d, R.ctr, R.Y4);
     k_pts_init<<<(B + 127) / 128, 128, 0, st>>>(B, R.S);
     k_active_view<<<(B + 127) / 128, 128, 0, st>>>(B, R.S, R.act);
     S_CUDA(cudaGetLastError());
