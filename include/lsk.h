@@ -141,6 +141,15 @@ int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t 
                            int32_t normalize_max, float* C, int64_t ldc, double* cmax_out, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* A host (pageable) cost matrix -> the padded device layout dst (row stride
+ * ldd floats, zero tail), fp64 sources rounded once to fp32 (solver.py:253) on
+ * the host: `threads` workers (0 = all cores) each round a row chunk into their
+ * own pinned buffer and copy it asynchronously while rounding the next; the
+ * copies are ordered before later work on `stream`. Replaces the pageable
+ * cudaMemcpy + device cast of CostMatrix.values (types.py:60-86). */
+int32_t lsk_h2d_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int32_t n, int32_t m, float* dst,
+                         int64_t ldd, int32_t threads, void* stream);
+
 /* The reference composition without materialising C64 on the host:
  * lsk_cost_range_f64 -> range_out[0] = max, range_out[1] = min of the fp64
  * cost (host doubles; CostMatrix.value_range = max - min, types.py:60-86;

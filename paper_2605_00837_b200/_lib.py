@@ -55,6 +55,7 @@ SIGNATURES = {
     "lsk_build_cost_workspace_bytes": (_c_sz, []),
     "lsk_build_cost_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_i32, _c_p, _c_i64, _c_p, _c_p,
                                     _c_sz, _c_p]),
+    "lsk_h2d_cost_f32": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_i32, _c_p]),
     "lsk_cost_range_f64": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_p, _c_p, _c_sz, _c_p]),
     "lsk_build_cost_div_f32": (_c_i32, [_c_p, _c_p, _c_i32, _c_i32, _c_i32, _c_dbl, _c_p, _c_i64, _c_p]),
     "lsk_cast_cost_f32": (_c_i32, [_c_p, _c_i32, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_p]),

@@ -357,13 +357,9 @@ int32_t run_solve(const SolveArgs& a, const Shard& sh, std::vector<Rank>& ranks,
       R.ghi = m;
     }
     R.leaf_lo = R.r * sh.spr;
-    S_CUDA(cudaMemsetAsync(R.F[0], 0, size_t(B) * sh.npad * 4, st));
-    S_CUDA(cudaMemsetAsync(R.G[0], 0, size_t(B) * sh.mpad * 4, st));
-    S_CUDA(cudaMemsetAsync(R.rowflag, 0, size_t(B) * (n > m ? n : m) * 4, st));
-    S_CUDA(cudaMemsetAsync(R.nflag, 0, 16, st));
-    S_CUDA(cudaMemsetAsync(R.bad, 0, size_t(B) * 4, st));
-    S_CUDA(cudaMemsetAsync(R.errrow, 0, size_t(B) * sh.npad * 4, st));
-    S_CUDA(cudaMemsetAsync(R.costrow, 0, size_t(B) * sh.npad * 4, st));
+    // potentials, flags, padded exchange slabs: all defined before any exchange
+    S_CUDA(cudaMemsetAsync(R.base + L.f0, 0, L.part - L.f0, st));
+    S_CUDA(cudaMemsetAsync(R.base + L.slots, 0, L.total - L.slots, st));
     lsk::k_pts_center<<<B, 256, 0, st>>>(a.X, a.Y, n, m, a.d, R.ctr);
     lsk::k_pts_pack<<<256, 256, 0, st>>>(a.X, (long long)B * n, n, a.d, R.ctr, R.X4);
     lsk::k_pts_pack<<<256, 256, 0, st>>>(a.Y, (long long)B * m, m, a.d, R.ctr, R.Y4);

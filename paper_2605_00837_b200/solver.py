@@ -90,7 +90,16 @@ def to_device_cost(cost):
     if isinstance(vals, np.ndarray):
         if vals.ndim != 2:
             raise DimensionMismatch("cost matrix must be 2-D")
-        src = torch.from_numpy(np.ascontiguousarray(vals)).to("cuda")
+        # host matrix: rounded to fp32 by the library's worker threads while the
+        # previous chunk is copied (lsk_h2d_cost_f32), straight into the padded layout
+        A = vals if vals.dtype in (np.float64, np.float32) else vals.astype(np.float64)
+        A = np.ascontiguousarray(A)
+        n, m = A.shape
+        ldc = (m + 3) // 4 * 4
+        out = torch.empty((n, ldc), dtype=torch.float32, device="cuda")
+        _lib.call("lsk_h2d_cost_f32", A.ctypes.data, int(A.dtype == np.float64), m, n, m, _ptr(out), ldc, 0,
+                  _stream_ptr(torch))
+        return DeviceCostMatrix(data=out, rows=n, cols=m)
     elif isinstance(vals, torch.Tensor):
         if vals.dim() != 2:
             raise DimensionMismatch("cost matrix must be 2-D")
