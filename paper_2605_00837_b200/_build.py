@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "liblsk.so")
 BUILD = os.path.join(ROOT, "build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
 UNITS = ["lsk_api.cu", "lsk_points.cu", "lsk_points_solve.cu", "lsk_h2d.cu", "lsk_dense_loop.cu", "lsk_f64.cu", "lsk_color.cu", "lsk_standard.cu", "lsk_reduce.cu", "lsk_diag.cu"]
 
 

@@ -98,6 +98,15 @@ struct DenseSolver {
   static constexpr int kRedComb = 4 * NW + 128;
   static constexpr size_t kRedFloats = 4 * NW + 128 + 64 * NW;
   // mbarriers: FULL[STAGES] (TMA) + SUMS[2] (per-step warp arrivals); then STAGES release counters
+  // LSK_X_ALLARRIVE (sanitizer builds only): every thread arrives on the row-sum
+  // mbarrier, so each reader's ordering before the next write / TMA refill is a
+  // direct arrive->wait edge instead of one composed through __syncwarp and the
+  // warp's lane-0 arrival (which racecheck does not compose)
+#ifdef LSK_X_ALLARRIVE
+  static constexpr int kSumArrivals = NT;
+#else
+  static constexpr int kSumArrivals = NW;
+#endif
   static constexpr size_t kSmemBytes = kRingBytes + kRedFloats * sizeof(float) + (STAGES + 2) * 8 + STAGES * 4 + 64;
 
   // ---- per-CTA state
@@ -181,8 +190,8 @@ struct DenseSolver {
     for (size_t k = threadIdx.x; k < kRingBytes / 16; k += NT) r4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (threadIdx.x == 0) {
       for (int s = 0; s < STAGES; ++s) mbar_init(&mbar[s], 1);
-      mbar_init(&bsum[0], NW);
-      mbar_init(&bsum[1], NW);
+      mbar_init(&bsum[0], kSumArrivals);
+      mbar_init(&bsum[1], kSumArrivals);
       for (int s = 0; s < STAGES; ++s) relc[s] = 0;
       fence_mbar_init();
     }
@@ -434,8 +443,13 @@ struct DenseSolver {
     if (lane == 0) {
       red[kRedRows + (step & 1) * NW + w] = s;
       if (check) red[kRedRows + 2 * NW + (step & 1) * NW + w] = z;
+#ifndef LSK_X_ALLARRIVE
       mbar_arrive(&bsum[step & 1]);
+#endif
     }
+#ifdef LSK_X_ALLARRIVE
+    mbar_arrive(&bsum[step & 1]);
+#endif
   }
   // block-barrier hand-off of the multiplicative pass: the warp sum goes to red
   // and the next step's __syncthreads publishes it (no mbarrier)

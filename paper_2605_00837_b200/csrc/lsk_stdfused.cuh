@@ -89,8 +89,13 @@ struct StdSolver {
     for (size_t k = threadIdx.x; k < kRingBytes / 16; k += NT) r4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (threadIdx.x == 0) {
       for (int s = 0; s < STAGES; ++s) mbar_init(&mbar[s], 1);
+#ifdef LSK_X_ALLARRIVE  // sanitizer builds: every thread arrives (see lsk_dense.cuh kSumArrivals)
+      mbar_init(&bsum[0], NT);
+      mbar_init(&bsum[1], NT);
+#else
       mbar_init(&bsum[0], NW);
       mbar_init(&bsum[1], NW);
+#endif
       fence_mbar_init();
     }
     __syncthreads();
@@ -115,8 +120,13 @@ struct StdSolver {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
       red[(step & 1) * NW + (threadIdx.x >> 5)] = s;
+#ifndef LSK_X_ALLARRIVE
       mbar_arrive(&bsum[step & 1]);
+#endif
     }
+#ifdef LSK_X_ALLARRIVE
+    mbar_arrive(&bsum[step & 1]);
+#endif
   }
   __device__ __forceinline__ float posted_sum(unsigned step) {
     mbar_wait(&bsum[step & 1], (step >> 1) & 1);
