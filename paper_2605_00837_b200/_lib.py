@@ -25,6 +25,7 @@ LSK_FLAG_NO_MULT = 32
 LSK_FLAG_STD_MULTIKERNEL = 64
 LSK_FLAG_SHARD_PARTIALS = 128
 LSK_FLAG_SHARD_ALLREDUCE = 256
+LSK_FLAG_NO_CLUSTER = 512
 LSK_SHARD_NONE = 0
 LSK_SHARD_OWNER = 1
 LSK_SHARD_PARTIALS = 2

@@ -7,6 +7,7 @@
 
 #include "../../include/lsk.h"
 #include "lsk_dense.cuh"
+#include "lsk_dense_cluster.cuh"
 #include "lsk_kernels.cuh"
 
 namespace {
@@ -105,6 +106,8 @@ struct DenseLayout {
   size_t off_f0, off_g0, zero_bytes, off_f1, off_g1, off_part, off_pairs, off_err, off_flag, off_redo, off_errrow, off_cost, total;
 };
 
+constexpr int kClusterMaxRows = 512;  // where the single-cluster solver beats the grid one (profiles/r2_c1_cluster.md)
+
 inline int dense_width(int m) {
   if (m <= 1024) return 1024;
   if (m <= 2048) return 2048;
@@ -133,6 +136,37 @@ DenseLayout dense_layout(int n, int m) {
   L.off_cost = o; o = align_up(o + size_t(L.G) * 4, 256);
   L.total = o;
   return L;
+}
+
+// small problems (m <= 1024, uniform targets): one cluster of 16 CTAs (8 where
+// a 16-CTA cluster cannot be scheduled), DSMEM exchanges, no grid barrier
+template <int CL>
+int32_t launch_cluster(lsk::DenseArgs& a, cudaStream_t st, bool& launched) {
+  using SV = lsk::ClusterSolver<CL>;
+  launched = false;
+  auto kern = k_solve_dense<SV>;
+  LSK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SV::kSmemBytes)));
+  if (CL > 8) LSK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(SV::NT);
+  cfg.dynamicSmemBytes = SV::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+    (void)cudaGetLastError();
+    return LSK_OK;  // not schedulable on this device: the caller falls back
+  }
+  LSK_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  launched = true;
+  return LSK_OK;
 }
 
 template <class SV>
@@ -221,7 +255,12 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   // multiplicative column update (lsk_dense.cuh, fused_pass_mult): large
   // problems at eps >= 1e-3 only; its extra rounding is relative to the f-side
   // argument scale, which only shows on degenerate tiny cases (g == 0 exactly)
-  a.mult = (a.stale && eps >= 1e-3 && (long long)n * m >= (1LL << 20) && !(flags & LSK_FLAG_NO_MULT)) ? 1 : 0;
+  // Its drift along the gauge direction grows with eps * K: pinned within the
+  // 1e-5 bar at the C2 class (eps = 1e-3, K = 1000: 6.5e-6, profiles/r2_parity_errors.jsonl),
+  // but at eps = 1e-2 it reaches 1.2e-5 on g by K = 300 (tests/test_gpu_cluster.py), so
+  // the gate is eps in [1e-3, 2e-3].
+  a.mult = (a.stale && eps >= 1e-3 && eps <= 2e-3 && (long long)n * m >= (1LL << 20) && !(flags & LSK_FLAG_NO_MULT))
+               ? 1 : 0;
   a.f0 = reinterpret_cast<float*>(ws + L.off_f0);
   a.f1 = reinterpret_cast<float*>(ws + L.off_f1);
   a.g0 = reinterpret_cast<float*>(ws + L.off_g0);
@@ -243,7 +282,15 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.out_cost = reinterpret_cast<float*>(hdr + 9);
   a.trace_iter = trace_iter;
   a.trace_err = trace_err;
-  if (flags & LSK_FLAG_UNIFORM_NU) {
+  bool done = false;
+  if ((flags & LSK_FLAG_UNIFORM_NU) && L.W == 1024 && n <= kClusterMaxRows && !(flags & LSK_FLAG_NO_CLUSTER)) {
+    lsk::DenseArgs ac = a;
+    ac.mult = 0;  // the cluster solver always runs the reference's direct g-side arithmetic
+    if ((rc = launch_cluster<16>(ac, st, done))) return rc;
+    if (!done && (rc = launch_cluster<8>(ac, st, done))) return rc;
+  }
+  if (done) {
+  } else if (flags & LSK_FLAG_UNIFORM_NU) {
     switch (L.W) {
       case 1024: rc = launch_dense<Solver1kU>(a, L.G, st); break;
       case 2048: rc = launch_dense<Solver2kU>(a, L.G, st); break;

@@ -146,7 +146,7 @@ def _uniform(log_w):
 
 
 def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None,
-                  uniform_nu=False, mult=True):
+                  uniform_nu=False, mult=True, cluster=True):
     C = to_device_cost(C)
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
@@ -164,6 +164,7 @@ def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
     flags |= _lib.LSK_FLAG_UNIFORM_NU if uniform_nu else 0
     flags |= 0 if mult else _lib.LSK_FLAG_NO_MULT
+    flags |= 0 if cluster else _lib.LSK_FLAG_NO_CLUSTER
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
     r.ev0.record()

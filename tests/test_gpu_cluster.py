@@ -1,0 +1,141 @@
+"""The single-cluster dense solver (csrc/lsk_dense_cluster.cuh): uniform
+targets, m <= 1024, n <= 512 run as ONE 16-CTA thread-block cluster with
+DSMEM exchanges instead of the 148-CTA grid solver (the reference golden
+fixtures of that size in test_gpu_parity.py also run through it).
+
+Checked against the oracle run live, against the grid solver on awkward
+shapes (one row, empty CTAs and warps, padded columns, the guard paths at
+small eps, early stops), with and without the stale shift; and the gate of
+the multiplicative column update, whose gauge drift left the 1e-5 bar at
+eps = 1e-2 (grid kernel, K = 300: g 1.2e-5 vs 3.2e-6 direct). Bars as in
+test_gpu_parity.py: potentials and cost within 1e-5 (per-potential max norm),
+identical status / iteration count / checkpoint iterations.
+"""
+
+import numpy as np
+import pytest
+
+import lsk_oracle as O
+import paper_2605_00837_b200 as lsk
+from conftest import golden, rel_max
+from paper_2605_00837_b200 import solver as S
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def launch(C, mu, nu, cfg, *, cluster, mult=True, stale=True):
+    import torch
+
+    lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
+    r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, stale=stale, uniform_nu=True, mult=mult, cluster=cluster)
+    torch.cuda.synchronize()
+    res = r.res.cpu().numpy()
+    nt = int(res[2])
+    return dict(f=r.f.cpu().numpy(), g=r.g.cpu().numpy(), status=int(res[0]), iters=int(res[1]),
+                trace=r.trace_iter[:nt].cpu().numpy().tolist(), err=float(r.resf[0].item()),
+                cost=float(r.resf[1].item()), guards=res[4:6].tolist())
+
+
+def test_c1_fixture(cuda_ok):
+    """C1 (n=m=1024, eps=1e-2, K=200) against the reference's own output through
+    the default path (the grid kernel; eps = 1e-2 is outside the multiplicative
+    update's gate, so the g-side arithmetic is the reference's)."""
+    z = golden("g1_c1_n1024")
+    X, Y = O.uniform_points(1024, 2, 0)
+    C = lsk.squared_euclidean_cost(X, Y)
+    w = lsk.make_distribution(np.ones(1024))
+    cfg = lsk.SinkhornConfig(epsilon=float(z["eps"]), tolerance=float(z["tol"]), max_iterations=int(z["K"]),
+                             check_interval=int(z["check"]))
+    r = launch(C, w, w, cfg, cluster=True)
+    assert r["iters"] == int(z["iterations"])
+    assert rel_max(r["f"], z["alpha"]) <= RTOL and rel_max(r["g"], z["beta"]) <= RTOL
+    assert abs(r["cost"] - float(z["cost"])) <= RTOL * abs(float(z["cost"]))
+
+
+@pytest.mark.parametrize("n", [512, 1024])
+def test_vs_oracle_k300(cuda_ok, n):
+    """n x 1024 at eps=1e-2, K=300 against the oracle (the reference's arithmetic):
+    n = 512 through the cluster kernel, n = 1024 through the grid kernel."""
+    rng = np.random.default_rng(5)
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (1024, 2))
+    C64 = O.sq_euclidean_cost(X, Y)
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, nu = lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(1024))
+    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=300)
+    r = launch(C, mu, nu, cfg, cluster=True)
+    ref = O.solve(C64, np.full(n, 1.0 / n), np.full(1024, 1.0 / 1024), 1e-2, tol=1e-30, max_iter=300)
+    assert r["iters"] == 300 and r["status"] == 0
+    assert rel_max(r["f"], ref["alpha"]) <= RTOL and rel_max(r["g"], ref["beta"]) <= RTOL, (
+        rel_max(r["f"], ref["alpha"]), rel_max(r["g"], ref["beta"]))
+    assert abs(r["cost"] - ref["cost"]) <= RTOL * abs(ref["cost"])
+
+
+def test_multiplicative_gate(cuda_ok):
+    """The multiplicative column update is gated to 1e-3 <= eps <= 2e-3: asking
+    for it at eps = 1e-2 runs the direct arithmetic (bit-identical results)."""
+    rng = np.random.default_rng(5)
+    X, Y = rng.uniform(0, 1, (1024, 2)), rng.uniform(0, 1, (1024, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    w = lsk.make_distribution(np.ones(1024))
+    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=40)
+    a = launch(C, w, w, cfg, cluster=False, mult=True)
+    b = launch(C, w, w, cfg, cluster=False, mult=False)
+    np.testing.assert_array_equal(a["f"], b["f"])
+    np.testing.assert_array_equal(a["g"], b["g"])
+
+
+SHAPES = [(1, 1024, 1e-2), (15, 1000, 1e-2), (16, 5, 5e-2), (17, 129, 1e-2), (300, 1021, 1e-3), (512, 1024, 1e-3),
+          (500, 640, 1e-4), (512, 1024, 2e-4)]
+
+
+@pytest.mark.parametrize("n,m,eps", SHAPES)
+def test_cluster_vs_grid_shapes(cuda_ok, n, m, eps):
+    """Against the grid solver: rows fewer than CTAs / warps, padded columns, eps
+    small enough for the row and column guards (exact in-warp row LSE, the exact
+    column pass merged warp -> CTA -> cluster)."""
+    rng = np.random.default_rng(n * 7 + m)
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, nu = lsk.make_distribution(rng.uniform(0.5, 1.5, n)), lsk.make_distribution(np.ones(m))
+    cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=60, check_interval=7)
+    a = launch(C, mu, nu, cfg, cluster=True)
+    b = launch(C, mu, nu, cfg, cluster=False)
+    assert (a["status"], a["iters"], a["trace"]) == (b["status"], b["iters"], b["trace"])
+    assert np.isfinite(a["f"]).all() and np.isfinite(a["g"]).all()
+    assert rel_max(a["f"], b["f"]) <= RTOL and rel_max(a["g"], b["g"]) <= RTOL, (rel_max(a["f"], b["f"]),
+                                                                                  rel_max(a["g"], b["g"]))
+    assert abs(a["cost"] - b["cost"]) <= RTOL * abs(b["cost"])
+
+
+def test_cluster_exact_variant_and_early_stop(cuda_ok):
+    """stale_shift=False (exact two-pass rows + the exact column pass every
+    iteration) and a tolerance met mid-run: same stop iteration, trace and
+    potentials of the returned iterate as the grid solver."""
+    rng = np.random.default_rng(3)
+    n, m = 512, 768
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, nu = lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(m))
+    for stale in (False, True):
+        cfg = lsk.SinkhornConfig(epsilon=5e-2, tolerance=1e-4, max_iterations=500, check_interval=5)
+        a = launch(C, mu, nu, cfg, cluster=True, stale=stale)
+        b = launch(C, mu, nu, cfg, cluster=False, stale=stale)
+        assert a["status"] == 1 and a["iters"] < 500
+        assert (a["status"], a["iters"], a["trace"]) == (b["status"], b["iters"], b["trace"])
+        assert rel_max(a["f"], b["f"]) <= RTOL and rel_max(a["g"], b["g"]) <= RTOL
+
+
+def test_cluster_bitwise_repeats(cuda_ok):
+    """Fixed-order reductions: repeated solves are bit-identical (reference
+    tests/test_solver.py:247-257)."""
+    rng = np.random.default_rng(9)
+    X, Y = rng.uniform(0, 1, (500, 2)), rng.uniform(0, 1, (1000, 2))
+    C = lsk.squared_euclidean_cost(X, Y)
+    mu, w = lsk.make_distribution(np.ones(500)), lsk.make_distribution(np.ones(1000))
+    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=50)
+    a = launch(C, mu, w, cfg, cluster=True)
+    b = launch(C, mu, w, cfg, cluster=True)
+    np.testing.assert_array_equal(a["f"], b["f"])
+    np.testing.assert_array_equal(a["g"], b["g"])
+    assert a["cost"] == b["cost"] and a["trace"] == b["trace"]

@@ -269,8 +269,8 @@ def test_uniform_nu_flag_bitwise_and_contract(cuda_ok):
         cfg = lsk.SinkhornConfig(epsilon=0.01, tolerance=1e-30, max_iterations=60, check_interval=7)
         lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
         out = []
-        for uni in (False, True):
-            r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=uni, mult=False)
+        for uni in (False, True):  # the grid kernels (the single-cluster one: tests/test_gpu_cluster.py)
+            r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=uni, mult=False, cluster=False)
             torch.cuda.synchronize()
             out.append((r.f.cpu().numpy(), r.g.cpu().numpy(), r.res.cpu().numpy(), r.resf.cpu().numpy()))
         for a, b in zip(out[0], out[1]):
@@ -297,8 +297,8 @@ def test_multiplicative_column_update_close_to_direct(cuda_ok, n, m, eps):
     cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=300)
     lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)
     out = []
-    for mult in (False, True):
-        r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=True, mult=mult)
+    for mult in (False, True):  # grid kernels; the single-cluster kernel: tests/test_gpu_cluster.py
+        r, _ = S._launch_solve(torch, C, lm, ln, w, cfg, uniform_nu=True, mult=mult, cluster=False)
         torch.cuda.synchronize()
         out.append((r.f.cpu().numpy(), r.g.cpu().numpy(), r.res.cpu().numpy(), r.resf.cpu().numpy()))
     (f0, g0, r0, c0), (f1, g1, r1, c1) = out
