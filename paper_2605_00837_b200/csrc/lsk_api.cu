@@ -375,7 +375,7 @@ int32_t lsk_update_beta_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   float2* pairs = static_cast<float2*>(workspace);
   dim3 grid((m + 1023) / 1024, parts);
   lsk::k_col_pairs<<<grid, 256, 0, S(stream)>>>(C, ldc, n, m, alpha, log_mu, ec.inv_eps, rs, pairs);
-  lsk::k_col_combine<<<(m + 255) / 256, 256, 0, S(stream)>>>(pairs, parts, m, ec.neg_eps, beta_out);
+  lsk::k_col_combine<<<(8 * m + 255) / 256, 256, 0, S(stream)>>>(pairs, parts, m, ec.neg_eps, beta_out);
   LSK_CUDA(cudaGetLastError());
   return LSK_OK;
 }

@@ -80,6 +80,20 @@ __global__ void k_loop_init(lsk::PtsState* st, int* act) {
   *act = 1;
 }
 __global__ void k_loop_active(const lsk::PtsState* st, int* act) { *act = st->active; }
+// LSK_FLAG_UNIFORM_NU contract (include/lsk.h): a non-uniform log nu ends the
+// solve as numerical_failure after 0 iterations (every later kernel sees act = 0)
+__global__ void k_loop_verify_uniform(const float* log_nu, int m, lsk::PtsState* st, int* act) {
+  const float L = log_nu[0];
+  int bad = 0;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) bad |= log_nu[j] != L;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) {
+    st->active = 0;
+    st->status = 2;
+    st->iters = 0;
+    st->err = NAN;
+    *act = 0;
+  }
+}
 __global__ void k_loop_results(const lsk::PtsState* st, int32_t* result, float* result_f, int cost) {
   const lsk::PtsState s = *st;
   result[LSK_RES_STATUS] = s.status;
@@ -124,12 +138,15 @@ int32_t solve_dense_loop(const float* C, int64_t ldc, int32_t n, int32_t m, cons
   L_CUDA(cudaMemsetAsync(G[0], 0, size_t(m) * 4, st));
   L_CUDA(cudaMemsetAsync(bad, 0, 16, st));
   k_loop_init<<<1, 1, 0, st>>>(S, act);
+  if (flags & LSK_FLAG_UNIFORM_NU) k_loop_verify_uniform<<<1, 1024, 0, st>>>(log_nu, m, S, act);
 
-  auto check = [&](int kk, bool final) -> int32_t {
+  // the checkpoint of iterate kk; `fused`: its per-row terms came with the stale row pass
+  auto check = [&](int kk, bool final, bool fused) -> int32_t {
     const float* fk = F[kk & 1];
     const float* gk = G[kk & 1];
-    lsk::k_row_lse<lsk::kRowCheck><<<n, 256, 0, st>>>(C, ldc, n, m, fk, gk, log_nu, log_mu, mu, inv_eps, neg_eps,
-                                                      rowterm, act);
+    if (!fused)
+      lsk::k_row_lse<lsk::kRowCheck><<<n, 256, 0, st>>>(C, ldc, n, m, fk, gk, log_nu, log_mu, mu, inv_eps, neg_eps,
+                                                        rowterm, act);
     lsk::k_pts_colcheck<<<dim3(8, 1), 256, 0, st>>>(1, n, fk, act, bad);
     lsk::k_pts_colcheck<<<dim3(8, 1), 256, 0, st>>>(1, m, gk, act, bad);
     lsk::k_pts_blocksum<<<dim3(nb, 1), 1024, 0, st>>>(1, n, 0, n, rowterm, act, blk);
@@ -142,25 +159,42 @@ int32_t solve_dense_loop(const float* C, int64_t ldc, int32_t n, int32_t m, cons
   const bool stale = (flags & LSK_FLAG_STALE_SHIFT) != 0;
   lsk_poll::StopPoll poll;
   if ((rc = poll.init(1, st))) return rc;
+  const bool uni = (flags & LSK_FLAG_UNIFORM_NU) != 0;
+  // one read of the row, shifted by the stale f (exact fallback per row); at a
+  // checkpoint the same read forms the check terms of iterate k-1
+  auto row_stale = [&](int k, bool chk) {
+    const float* fp = F[(k - 1) & 1];
+    const float* gp = G[(k - 1) & 1];
+    float* fn = F[k & 1];
+    if (chk && uni)
+      lsk::k_row_alpha_stale<true, true><<<n, 256, 0, st>>>(C, ldc, n, m, fp, gp, log_nu, inv_eps, neg_eps, fn, act,
+                                                            log_mu, mu, rowterm);
+    else if (chk)
+      lsk::k_row_alpha_stale<true, false><<<n, 256, 0, st>>>(C, ldc, n, m, fp, gp, log_nu, inv_eps, neg_eps, fn, act,
+                                                             log_mu, mu, rowterm);
+    else if (uni)
+      lsk::k_row_alpha_stale<false, true><<<n, 256, 0, st>>>(C, ldc, n, m, fp, gp, log_nu, inv_eps, neg_eps, fn, act);
+    else
+      lsk::k_row_alpha_stale<false, false><<<n, 256, 0, st>>>(C, ldc, n, m, fp, gp, log_nu, inv_eps, neg_eps, fn, act);
+  };
   for (int k = 1; k <= K; ++k) {
-    if (k > 1 && (k - 1) % c == 0) {
-      if ((rc = check(k - 1, false))) return rc;
+    const bool chk = k > 1 && (k - 1) % c == 0;
+    if (k > 1 && stale) row_stale(k, chk);
+    if (chk) {
+      if ((rc = check(k - 1, false, stale))) return rc;
       bool stop = false;
       if ((rc = poll.after_check(act, st, stop))) return rc;
       if (stop) break;
     }
-    if (k > 1 && stale)  // one read of the row, shifted by the stale f (exact fallback per row)
-      lsk::k_row_alpha_stale<<<n, 256, 0, st>>>(C, ldc, n, m, F[(k - 1) & 1], G[(k - 1) & 1], log_nu, inv_eps, neg_eps,
-                                                F[k & 1], act);
-    else
+    if (!(k > 1 && stale))
       lsk::k_row_lse<lsk::kRowAlpha><<<n, 256, 0, st>>>(C, ldc, n, m, nullptr, G[(k - 1) & 1], log_nu, nullptr,
                                                         nullptr, inv_eps, neg_eps, F[k & 1], act);
     lsk::k_col_pairs<<<dim3((m + 1023) / 1024, parts), 256, 0, st>>>(C, ldc, n, m, F[k & 1], log_mu, inv_eps, rs,
                                                                     pairs, act);
-    lsk::k_col_combine<<<(m + 255) / 256, 256, 0, st>>>(pairs, parts, m, neg_eps, G[k & 1], act);
+    lsk::k_col_combine<<<(8 * m + 255) / 256, 256, 0, st>>>(pairs, parts, m, neg_eps, G[k & 1], act);
     L_CUDA(cudaGetLastError());
   }
-  if ((rc = check(K, true))) return rc;
+  if ((rc = check(K, true, false))) return rc;
   lsk::k_pts_pick<<<dim3(64, 1), 256, 0, st>>>(1, n, F[0], F[1], S, f_out);
   lsk::k_pts_pick<<<dim3(64, 1), 256, 0, st>>>(1, m, G[0], G[1], S, g_out);
   if (flags & LSK_FLAG_COST) {
