@@ -253,7 +253,7 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.stale = (flags & LSK_FLAG_STALE_SHIFT) ? 1 : 0;
   a.want_cost = (flags & LSK_FLAG_COST) ? 1 : 0;
   // multiplicative column update (lsk_dense.cuh, fused_pass_mult): large
-  // problems at eps >= 1e-3 only; its extra rounding is relative to the f-side
+  // problems at 1e-3 <= eps <= 2e-3 only; its extra rounding is relative to the f-side
   // argument scale, which only shows on degenerate tiny cases (g == 0 exactly)
   // Its drift along the gauge direction grows with eps * K: pinned within the
   // 1e-5 bar at the C2 class (eps = 1e-3, K = 1000: 6.5e-6, profiles/r2_parity_errors.jsonl),

@@ -28,7 +28,7 @@
 //    A grid-wide fixed-order combine of the G per-CTA column partials forms
 //    g^k. Sums outside [1e-20, 1e30] fall back to the exact max shift (rows:
 //    from the smem copy of the row; columns: an exact (max, sumexp) pass).
-//  * Uniform targets, eps >= 1e-3, n m >= 2^20 (fused_pass_mult): the g-side
+//  * Uniform targets, 1e-3 <= eps <= 2e-3, n m >= 2^20 (fused_pass_mult): the g-side
 //    term of (i, j) is the f-side term times 2^(a_i + b) in exact arithmetic,
 //    so the column update is one FFMA2 per pair from the f-side terms kept in
 //    registers (no second cost read, no second ex2); a block barrier per row.
@@ -601,10 +601,11 @@ struct DenseSolver {
   // update of row q-1 needs no cost element and no ex2: one FFMA2 per pair
   // from the f-side terms kept in registers (uniform nu only: b_j is one scalar). It is used for a row
   // only while a_i stays in a band where no f-side term that underflowed could
-  // matter to a column sum inside the guard band, and only when eps >= 1e-3
+  // matter to a column sum inside the guard band, and only when 1e-3 <= eps <= 2e-3
   // (a.mult); otherwise the row takes the direct update. The exponents carry
   // the f-side argument rounding instead of the g-side one (|dy| <= |y| 2^-24):
-  // parity with the reference stays within the fp32 tolerance at eps >= 1e-3.
+  // parity with the reference stays within the fp32 tolerance there (its gauge
+  // drift grows with eps * K: 1.2e-5 at eps = 1e-2, K = 300, profiles/r2_c1_cluster.md).
   __device__ __forceinline__ void f_part_e(const float* row, float fold, float& s, f2 (&e)[P2]) const {
     f2 c[P2];
     load_row(row, c);

@@ -4,7 +4,7 @@ restatement of the reference), at fixed iteration counts so the comparison is
 about the potentials, not the stop decision. Covers the kernel variants the
 dispatcher picks by shape: uniform / general targets, column padding, 1 to
 hundreds of rows per CTA, the multiplicative column update (n*m >= 2^20,
-eps >= 1e-3) and the exact first iteration."""
+1e-3 <= eps <= 2e-3) and the exact first iteration."""
 
 import numpy as np
 import pytest

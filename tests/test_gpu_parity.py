@@ -281,9 +281,9 @@ def test_uniform_nu_flag_bitwise_and_contract(cuda_ok):
     assert res[0] == 2 and res[1] == 0
 
 
-@pytest.mark.parametrize("n,m,eps", [(8192, 8192, 1e-3), (1024, 1024, 1e-2), (4096, 2048, 2e-3)])
+@pytest.mark.parametrize("n,m,eps", [(8192, 8192, 1e-3), (1024, 1024, 1.5e-3), (4096, 2048, 2e-3)])
 def test_multiplicative_column_update_close_to_direct(cuda_ok, n, m, eps):
-    """The multiplicative column update (uniform nu, n*m >= 2^20, eps >= 1e-3) against the
+    """The multiplicative column update (uniform nu, n*m >= 2^20, 1e-3 <= eps <= 2e-3) against the
     direct g-side arithmetic on the same problem: potentials within the fp32 parity
     tolerance, same status and iteration count, cost to 1e-6."""
     import torch
