@@ -238,6 +238,14 @@ int32_t lsk_materialize_plan_f64(const double* C, int64_t ldc, int32_t n, int32_
  */
 #define LSK_FLAG_SHARD_PARTIALS 128
 #define LSK_FLAG_SHARD_ALLREDUCE 256
+/* CUDA graphs: after the first checkpoint the iteration loop is captured as
+ * blocks of check_interval iterations and replayed (single-GPU, batched and
+ * emulated solves, when there are >= 3 blocks and the caller is not already
+ * capturing the stream). LSK_FLAG_NO_GRAPH enqueues every iteration;
+ * LSK_FLAG_GRAPH_NCCL also captures the NCCL collectives of a sharded solve
+ * (opt-in: not validated on a multi-GPU box by this build). */
+#define LSK_FLAG_NO_GRAPH 1024
+#define LSK_FLAG_GRAPH_NCCL 2048
 #define LSK_SHARD_NONE 0
 #define LSK_SHARD_OWNER 1
 #define LSK_SHARD_PARTIALS 2

@@ -26,6 +26,8 @@ LSK_FLAG_STD_MULTIKERNEL = 64
 LSK_FLAG_SHARD_PARTIALS = 128
 LSK_FLAG_SHARD_ALLREDUCE = 256
 LSK_FLAG_NO_CLUSTER = 512
+LSK_FLAG_NO_GRAPH = 1024
+LSK_FLAG_GRAPH_NCCL = 2048
 LSK_SHARD_NONE = 0
 LSK_SHARD_OWNER = 1
 LSK_SHARD_PARTIALS = 2

@@ -410,10 +410,14 @@ struct PtsState {
 // check decision for every problem (solver.py:286-300): err = fixed-order sum
 // of the row-block sums; stop on non-finite f/g, non-finite err or err < tol.
 // kk = the iterate being checked; final = the check at the cap.
+// kk_dev (optional): the checked iterate read from the device (a CUDA-graph
+// replay of a block of iterations cannot carry it as a launch parameter)
 static __global__ void k_pts_decide(int B, int n, const float* __restrict__ blk, int* bad, double tol, int kk, int final,
-                             PtsState* st, int* trace_iter, float* trace_err, int cap) {
+                             PtsState* st, int* trace_iter, float* trace_err, int cap,
+                             const int* __restrict__ kk_dev = nullptr) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
+  if (kk_dev) kk = *kk_dev;
   PtsState& s = st[b];
   if (!s.active) return;
   const int nb = (n + kPtsBlk - 1) / kPtsBlk;

@@ -32,6 +32,16 @@
 // check's error and the transport cost sum fixed 1024-row blocks of per-row
 // terms, independent of P.
 //
+// CUDA graphs: after the first checkpoint the loop is a repetition of blocks
+// of c iterations (the block's first iteration carries the check of the
+// previous iterate), so one block is captured once (two when c is odd: the
+// potential buffers alternate with the iteration's parity) and replayed; the
+// checked iterate reaches k_pts_decide through a device counter that the
+// block's first node advances. The host poll runs between replays. Single-GPU
+// and emulated solves use graphs by default; with an NCCL communicator they
+// are opt-in (LSK_FLAG_GRAPH_NCCL: NCCL calls captured into the graph), and
+// LSK_FLAG_NO_GRAPH enqueues every iteration.
+//
 // lsk_solve_points_emulated_f32 runs the same decomposition for P virtual
 // ranks on one GPU: each rank has its own workspace, the rank-local kernels of
 // every phase run rank after rank on one stream, and the collectives become
@@ -119,7 +129,7 @@ int32_t make_shard(int n, int m, int P, int mode, Shard& s) {
 
 struct PtsLayout {
   size_t x4, y4, ctr, f0, f1, g0, g1, fsel, gsel, part, slots, rowflag, nflag, errrow, errblk, bad, badslots, costrow, costblk, state,
-      act, total;
+      act, kk, total;
 };
 
 PtsLayout pts_layout(int B, int n, int m, const Shard& s) {
@@ -150,6 +160,7 @@ PtsLayout pts_layout(int B, int n, int m, const Shard& s) {
   L.costblk = o; o = al(o + size_t(B) * nb * 4);
   L.state = o; o = al(o + size_t(B) * sizeof(lsk::PtsState));
   L.act = o; o = al(o + size_t(B) * 4);
+  L.kk = o; o = al(o + 16);
   L.total = o;
   return L;
 }
@@ -246,6 +257,7 @@ struct Rank {
   float *costrow, *costblk;
   lsk::PtsState* S;
   int* act;
+  int* kk;        // graph replay: the iterate the next check decides on
   int rlo, rhi;   // f rows (source points)
   int glo, ghi;   // g rows (target points) this rank finishes
   int leaf_lo;    // partials: first source chunk it reduces
@@ -274,7 +286,30 @@ void carve(Rank& R, char* ws, const PtsLayout& L) {
   R.costblk = reinterpret_cast<float*>(ws + L.costblk);
   R.S = reinterpret_cast<lsk::PtsState*>(ws + L.state);
   R.act = reinterpret_cast<int*>(ws + L.act);
+  R.kk = reinterpret_cast<int*>(ws + L.kk);
 }
+
+__global__ void k_add_int(int* p, int v) { *p += v; }
+
+// The stream captures are recorded on: the caller's stream may be the legacy
+// default stream, which cannot be captured (the graph is launched on it).
+// One non-blocking stream per host thread and device, kept for the process.
+struct CaptureStream {
+  cudaStream_t s = nullptr;
+  int device = -1;
+};
+inline thread_local CaptureStream t_cap;
+int32_t capture_stream(cudaStream_t& out) {
+  int dev = 0;
+  S_CUDA(cudaGetDevice(&dev));
+  if (t_cap.s == nullptr || t_cap.device != dev) {
+    S_CUDA(cudaStreamCreateWithFlags(&t_cap.s, cudaStreamNonBlocking));
+    t_cap.device = dev;
+  }
+  out = t_cap.s;
+  return LSK_OK;
+}
+__global__ void k_set_int(int* p, int v) { *p = v; }
 
 // The collectives of the decomposition. Every exchanged buffer sits at the
 // same workspace offset on every rank, rank r's contribution at
@@ -442,6 +477,7 @@ int32_t run_solve(const SolveArgs& a, const Shard& sh, std::vector<Rank>& ranks,
   auto pot_off = [&](float* p, const Rank& R) { return size_t(reinterpret_cast<char*>(p) - R.base); };
 
   // check decision for iterate kk from the f-half's row terms
+  bool dev_kk = false;  // inside a captured block: the checked iterate comes from R.kk
   auto decide = [&](int kk, int gbuf, bool final) -> int32_t {
     for (Rank& R : ranks) {
       lsk::k_pts_colcheck<<<dim3(8, B), 256, 0, st>>>(B, m, R.G[gbuf], R.act, R.bad);
@@ -458,16 +494,15 @@ int32_t run_solve(const SolveArgs& a, const Shard& sh, std::vector<Rank>& ranks,
     for (Rank& R : ranks) {
       lsk::k_pts_blocksum<<<dim3(nb, B), 1024, 0, st>>>(B, n, 0, n, R.errrow, R.act, R.errblk);
       lsk::k_pts_decide<<<(B + 127) / 128, 128, 0, st>>>(B, n, R.errblk, R.bad, a.tol, kk, final ? 1 : 0, R.S,
-                                                          a.trace_iter, a.trace_err, cap);
+                                                          a.trace_iter, a.trace_err, cap, dev_kk ? R.kk : nullptr);
       k_active_view<<<(B + 127) / 128, 128, 0, st>>>(B, R.S, R.act);
       S_CUDA(cudaGetLastError());
     }
     return LSK_OK;
   };
 
-  lsk_poll::StopPoll poll;
-  S_TRY(poll.init(B, st));
-  for (int k = 1; k <= a.max_iter; ++k) {
+  // one iteration k (everything but the host poll)
+  auto iterate = [&](int k) -> int32_t {
     const bool do_check = (k > 1) && ((k - 1) % a.check == 0);
     const int pb = (k - 1) & 1, nbuf = k & 1;
     const bool st_k = stale && k > 1;
@@ -517,10 +552,88 @@ int32_t run_solve(const SolveArgs& a, const Shard& sh, std::vector<Rank>& ranks,
         if (st_k) S_TRY(run_fixup(R, hg, 0, m, a.log_mu));
       }
     }
-    if (do_check) {
+    return LSK_OK;
+  };
+
+  lsk_poll::StopPoll poll;
+  S_TRY(poll.init(B, st));
+  const int c = a.check;
+  // graph blocks start at the first checkpoint iteration c + 1 and repeat every c
+  const int first_blk = c + 1;
+  const int nblk = a.max_iter >= first_blk ? (a.max_iter - first_blk + 1) / c : 0;
+  bool graphs = !(a.flags & LSK_FLAG_NO_GRAPH) && (X.nc == nullptr || (a.flags & LSK_FLAG_GRAPH_NCCL)) && nblk >= 3;
+  if (graphs) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    S_CUDA(cudaStreamIsCapturing(st, &cs));
+    graphs = cs == cudaStreamCaptureStatusNone;  // a caller's capture already owns the stream
+  }
+  const int graph_end = graphs ? first_blk + nblk * c : 1;  // iterations [first_blk, graph_end) replayed
+  bool stopped = false;
+  for (int k = 1; k <= a.max_iter && !stopped; ++k) {
+    if (graphs && k == first_blk) break;
+    S_TRY(iterate(k));
+    if ((k > 1) && ((k - 1) % c == 0)) {
       bool stop = false;
       S_TRY(poll.after_check(ranks[0].act, st, stop));
-      if (stop) break;
+      if (stop) stopped = true;
+    }
+  }
+  if (graphs && !stopped) {
+    cudaGraphExec_t ge[2] = {nullptr, nullptr};
+    auto destroy = [&]() {
+      for (auto& e : ge)
+        if (e) cudaGraphExecDestroy(e);
+    };
+    // capture block b's shape: iterations first_blk + b c ... + c - 1
+    // every launcher above enqueues on `st` / X.s: point them at the capture stream
+    // while recording, back at the caller's stream for the replays
+    auto capture = [&](int b, cudaGraphExec_t* out) -> int32_t {
+      const int k0 = first_blk + b * c;
+      cudaGraph_t g = nullptr;
+      cudaStream_t cap = nullptr;
+      S_TRY(capture_stream(cap));
+      const cudaStream_t main_st = st;
+      S_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed));
+      st = cap;
+      X.s = cap;
+      int32_t rc = LSK_OK;
+      dev_kk = true;
+      for (Rank& R : ranks) k_add_int<<<1, 1, 0, st>>>(R.kk, c);
+      for (int k = k0; k < k0 + c && rc == LSK_OK; ++k) rc = iterate(k);
+      dev_kk = false;
+      st = main_st;
+      X.s = main_st;
+      const cudaError_t ec = cudaStreamEndCapture(cap, &g);
+      if (rc != LSK_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      S_CUDA(ec);
+      const cudaError_t ei = cudaGraphInstantiate(out, g, 0);
+      cudaGraphDestroy(g);
+      S_CUDA(ei);
+      return LSK_OK;
+    };
+    int32_t rc = LSK_OK;
+    for (Rank& R : ranks) k_set_int<<<1, 1, 0, st>>>(R.kk, first_blk - 1 - c);
+    const int nshape = (c & 1) ? 2 : 1;
+    for (int q = 0; q < nshape && rc == LSK_OK; ++q) rc = capture(q, &ge[q]);
+    for (int b = 0; b < nblk && rc == LSK_OK && !stopped; ++b) {
+      const cudaError_t e = cudaGraphLaunch(ge[b % nshape], st);
+      if (e != cudaSuccess) rc = sfail(LSK_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+      bool stop = false;
+      if (rc == LSK_OK) rc = poll.after_check(ranks[0].act, st, stop);
+      stopped = stop;
+    }
+    destroy();
+    S_TRY(rc);
+    for (int k = graph_end; k <= a.max_iter && !stopped; ++k) {
+      S_TRY(iterate(k));
+      if ((k - 1) % c == 0) {
+        bool stop = false;
+        S_TRY(poll.after_check(ranks[0].act, st, stop));
+        if (stop) stopped = true;
+      }
     }
   }
   // the final check at the cap (solver.py:286-316): a check-only f pass of iterate K

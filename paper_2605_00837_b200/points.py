@@ -134,7 +134,7 @@ def _expansion_ok(Xb, Yb, eps, normalize):
 
 
 def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=False, shard="partials",
-            emulate_ranks=None):
+            emulate_ranks=None, graphs=True):
     torch = _torch()
     if config.precision != "single":
         raise NotImplementedError("the on-the-fly points solver computes in fp32; use precision='single', or "
@@ -191,6 +191,10 @@ def _launch(X, Y, mu, nu, config, normalize, stale, want_cost, comm, expansion=F
         expansion = False
     flags |= _lib.LSK_FLAG_EXPANSION if expansion else 0
     flags |= shard_flag
+    # CUDA-graph replay of the iteration blocks (include/lsk.h): the library's default,
+    # off with graphs=False, NCCL collectives captured too with graphs="nccl"
+    flags |= _lib.LSK_FLAG_NO_GRAPH if graphs is False else 0
+    flags |= _lib.LSK_FLAG_GRAPH_NCCL if graphs == "nccl" else 0
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
     r.mismatch = None
@@ -233,7 +237,7 @@ def _reports(r, return_device=False):
 
 
 def solve_points_otf(X, Y, mu, nu, config, normalize="none", *, stale_shift=True, comm=None, return_device=False,
-                     expansion=False, shard="partials"):
+                     expansion=False, shard="partials", graphs=True):
     """One on-the-fly solve of points X (n, d) vs Y (m, d); see module doc.
     ``expansion=True`` (opt-in speed mode) evaluates the cost as
     |x|^2+|y|^2-2x.y in the stale sweeps when eps >= 5e-3 and the rounding
@@ -241,28 +245,30 @@ def solve_points_otf(X, Y, mu, nu, config, normalize="none", *, stale_shift=True
     FP32 ops per pair). Its cancellation moves the potentials by up to ~3e-5
     (per potential) on the C5 shape -- outside the 1e-5 parity bar -- so the
     default is the direct form.
-    ``comm`` / ``shard``: see the module doc."""
-    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, comm, expansion, shard)
+    ``comm`` / ``shard``: see the module doc. ``graphs``: CUDA-graph replay of the
+    iteration blocks (True: the library default; False: off; "nccl": also capture
+    the collectives of a sharded solve)."""
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, comm, expansion, shard, graphs=graphs)
     return _reports(r, return_device)[0]
 
 
 def solve_points_emulated(X, Y, mu, nu, config, ranks, normalize="none", *, shard="partials", stale_shift=True,
-                          expansion=False):
+                          expansion=False, graphs=True):
     """The P-rank decomposition of ``solve_points_otf(..., comm=<P ranks>,
     shard=shard)`` run on this one GPU: every virtual rank has its own
     workspace, its kernels run rank after rank, and the collectives are device
     copies (``lsk_solve_points_emulated_f32``). Returns ``(report, potentials,
     rank_mismatch)`` -- rank 0's results and the number of ranks whose returned
     potentials / status / error / cost differ from rank 0's in any bit."""
-    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, None, expansion, shard, ranks)
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, None, expansion, shard, ranks, graphs=graphs)
     rep, pot = _reports(r)[0]
     return rep, pot, int(r.mismatch.item())
 
 
 def solve_points_batched(X, Y, config, mu=None, nu=None, normalize="none", *, stale_shift=True,
-                         return_device=False, expansion=False):
+                         return_device=False, expansion=False, graphs=True):
     """B independent solves, X (B, n, d) vs Y (B, m, d), uniform marginals by
     default (``mu``/``nu``: a DiscreteDistribution for all, or one per problem).
     Returns a list of (SolveReport, DualPotentials)."""
-    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, None, expansion)
+    r = _launch(X, Y, mu, nu, config, normalize, stale_shift, True, None, expansion, graphs=graphs)
     return _reports(r, return_device)

@@ -33,17 +33,19 @@ def main():
     base = r1.device_seconds / a.iters
     print(f"C4 rigid pair n=m={a.n}, eps=1e-3, {a.iters} iterations, one B200; unsharded: "
           f"{base * 1e3:.3f} ms/iteration\n")
-    print("| design | P | device ms / iteration (all ranks, serial) | per-rank estimate (/P) | "
+    print("| design | P | CUDA graphs | device ms / iteration (all ranks, serial) | per-rank estimate (/P) | "
           "ideal (unsharded / P) | per-rank overhead | bitwise = unsharded | ranks agree |")
-    print("|---|---|---|---|---|---|---|---|")
+    print("|---|---|---|---|---|---|---|---|---|")
     for shard in ("partials", "owner", "allreduce"):
         for P in (1, 2, 4, 8):
-            PT.solve_points_emulated(X, Y, None, None, cfg, P, "max", shard=shard)
-            r, p, mism = PT.solve_points_emulated(X, Y, None, None, cfg, P, "max", shard=shard)
-            t = r.device_seconds / a.iters
-            same = bool(np.array_equal(p.alpha, p1.alpha) and np.array_equal(p.beta, p1.beta))
-            print(f"| {shard} | {P} | {t * 1e3:.3f} | {t / P * 1e3:.3f} | {base / P * 1e3:.3f} | "
-                  f"{(t / P - base / P) / (base / P) * 100:+.1f}% | {same} | {mism == 0} |", flush=True)
+            for graphs in (True, False):
+                PT.solve_points_emulated(X, Y, None, None, cfg, P, "max", shard=shard, graphs=graphs)
+                r, p, mism = PT.solve_points_emulated(X, Y, None, None, cfg, P, "max", shard=shard, graphs=graphs)
+                t = r.device_seconds / a.iters
+                same = bool(np.array_equal(p.alpha, p1.alpha) and np.array_equal(p.beta, p1.beta))
+                print(f"| {shard} | {P} | {'on' if graphs else 'off'} | {t * 1e3:.3f} | {t / P * 1e3:.3f} | "
+                      f"{base / P * 1e3:.3f} | {(t / P - base / P) / (base / P) * 100:+.1f}% | {same} | {mism == 0} |",
+                      flush=True)
 
 
 if __name__ == "__main__":
