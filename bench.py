@@ -392,9 +392,12 @@ def c2_line(args, clocks_index):
         rep, pot = lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=not args.direct)
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
-    e2e = {"value": K * e2e_steps / t_e2e, "unit": "iters/s", "h2d_bytes_per_step": N * N * 8 + 3 * N * 4,
+    # bytes over PCIe: the fp64 host matrix is rounded to fp32 on the host cores (solver.py:253
+    # restated by lsk_h2d_cost_f32) and copied as fp32, plus log mu / log nu / mu
+    e2e = {"value": K * e2e_steps / t_e2e, "unit": "iters/s", "h2d_bytes_per_step": N * N * 4 + 3 * N * 4,
            "d2h_bytes_per_step": 2 * N * 4 + 8 * 4 + 2 * 4 + (K // CHECK + 1) * 8,
-           "path": "paper_2605_00837_b200.solve(CostMatrix(numpy fp64, pageable host), ...) -> numpy potentials",
+           "path": "paper_2605_00837_b200.solve(CostMatrix(numpy fp64, pageable host), ...) -> numpy potentials; "
+                   "the 512 MiB fp64 host matrix is rounded to fp32 by host threads and copied in pinned chunks",
            "steps": e2e_steps}
 
     # ---- roofline of the persistent solver kernel

@@ -228,6 +228,40 @@ def test_dense_wide_loop_path(cuda_ok):
         assert abs(rep.transport_cost - r["cost"]) <= RTOL * abs(r["cost"])
 
 
+def test_dense_wide_loop_uniform(cuda_ok):
+    """m > 8192 with uniform targets: the loop's uniform row kernels (log nu read
+    once) and the checkpoint terms fused into the stale row pass, against the
+    oracle; and the uniform-flag contract there (a non-uniform log nu ends the
+    solve as numerical_failure after 0 iterations)."""
+    import torch
+
+    from paper_2605_00837_b200 import solver as S
+
+    rng = np.random.default_rng(11)
+    n, m = 200, 9000
+    X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+    C64 = O.sq_euclidean_cost(X, Y)
+    mu_w = rng.uniform(0.5, 1.5, n)
+    mu_w /= mu_w.sum()
+    nu_w = np.full(m, 1.0 / m)
+    for K, tol in ((43, 1e-30), (400, 1e-4)):
+        r = O.solve(C64, mu_w, nu_w, 0.02, tol=tol, max_iter=K, check=10)
+        rep, pot = lsk.solve(lsk.CostMatrix(values=C64), dist(mu_w), lsk.make_distribution(np.ones(m)),
+                             lsk.SinkhornConfig(epsilon=0.02, tolerance=tol, max_iterations=K))
+        assert rep.status == r["status"] and rep.iterations == r["iterations"]
+        assert [k for k, _ in rep.error_trace] == [int(k) for k, _ in r["trace"]]
+        assert rel_max(pot.alpha, r["alpha"]) <= RTOL and rel_max(pot.beta, r["beta"]) <= RTOL
+        assert abs(rep.transport_cost - r["cost"]) <= RTOL * abs(r["cost"])
+    C = lsk.squared_euclidean_cost(X, Y)
+    cfg = lsk.SinkhornConfig(epsilon=0.02, tolerance=1e-30, max_iterations=20)
+    mu = lsk.make_distribution(mu_w)
+    bad_nu = lsk.make_distribution(rng.uniform(0.5, 1.5, m))
+    r, _ = S._launch_solve(torch, C, S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, bad_nu.log_weights),
+                           S._dev_f32(torch, mu.weights), cfg, uniform_nu=True)
+    res = r.res.cpu().numpy()
+    assert res[0] == 2 and res[1] == 0
+
+
 def test_argument_build_bitwise(cuda_ok):
     """The packed argument builder reproduces numpy's separately rounded fp32
     ops bit for bit (solver.py:77-79; an FMA here breaks eps=1e-4)."""
