@@ -24,21 +24,24 @@ def main():
     t0 = time.time()
     kinds = {}
     for it in range(count):
-        kind = rng.choice(["dense", "dense_uni", "wide", "exact", "points", "batched", "standard", "double"])
+        kind = rng.choice(["dense", "dense_uni", "wide", "exact", "points", "batched", "standard", "double",
+                           "cluster", "points_long"])
         n = int(rng.integers(1, 3000))
         m = int(rng.integers(1, 8192)) if kind != "wide" else int(rng.integers(8193, 12000))
         if kind == "wide":
             n = int(rng.integers(1, 600))
+        if kind == "cluster":  # the single-cluster solver's range (uniform targets, n <= 512, m <= 1024)
+            n, m = int(rng.integers(1, 513)), int(rng.integers(1, 1025))
         eps = float(rng.choice([1e-3, 3e-3, 1e-2, 0.1]))
-        K = int(rng.integers(1, 30))
+        K = int(rng.integers(1, 30)) if kind != "points_long" else int(rng.integers(40, 120))
         c = int(rng.integers(1, 8))
         cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=float(rng.choice([1e-30, 1e-4])), max_iterations=K,
                                  check_interval=c, precision="double" if kind == "double" else "single")
         X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
-        if kind in ("points", "batched"):
+        if kind in ("points", "batched", "points_long"):
             n, m = min(n, 2000), min(m, 3000)
             X, Y = X[:n], Y[:m]
-            if kind == "points":
+            if kind in ("points", "points_long"):
                 rep, pot = PT.solve_points_otf(X, Y, None, None, cfg, normalize=rng.choice(["none", "max"]))
             else:
                 B = int(rng.integers(1, 5))
@@ -51,6 +54,8 @@ def main():
                 X, Y = X[:n], Y[:m]
             C = lsk.squared_euclidean_cost(X, Y)
             mu = lsk.make_distribution(np.ones(n) if kind in ("dense_uni", "wide") else rng.uniform(0.5, 1.5, n))
+            if kind == "wide" and rng.uniform() < 0.5:
+                mu = lsk.make_distribution(rng.uniform(0.5, 1.5, n))
             nu = lsk.make_distribution(np.ones(m) if kind != "dense" else rng.uniform(0.5, 1.5, m))
             if kind == "standard":
                 rep, u, v = lsk.solve_standard_domain(C, mu, nu, cfg)
