@@ -1,6 +1,7 @@
 // C-ABI implementation (include/lsk.h): argument checks, workspace carving,
 // launch configuration. All compute lives in lsk_dense.cuh / lsk_kernels.cuh.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -120,6 +121,9 @@ DenseLayout dense_layout(int n, int m) {
   DenseLayout L{};
   L.W = dense_width(m);
   L.G = num_sms();
+#ifdef LSK_X_GRID_ENV
+  if (const char* e = getenv("LSK_DENSE_GRID")) L.G = atoi(e);
+#endif
   if (n < L.G) L.G = n > 0 ? n : 1;
   size_t o = kHeaderInts * 4;
   L.off_f0 = o; o = align_up(o + size_t(n) * 4, 256);

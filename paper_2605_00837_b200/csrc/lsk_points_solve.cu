@@ -618,16 +618,28 @@ int32_t run_solve(const SolveArgs& a, const Shard& sh, std::vector<Rank>& ranks,
     for (Rank& R : ranks) k_set_int<<<1, 1, 0, st>>>(R.kk, first_blk - 1 - c);
     const int nshape = (c & 1) ? 2 : 1;
     for (int q = 0; q < nshape && rc == LSK_OK; ++q) rc = capture(q, &ge[q]);
-    for (int b = 0; b < nblk && rc == LSK_OK && !stopped; ++b) {
-      const cudaError_t e = cudaGraphLaunch(ge[b % nshape], st);
-      if (e != cudaSuccess) rc = sfail(LSK_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
-      bool stop = false;
-      if (rc == LSK_OK) rc = poll.after_check(ranks[0].act, st, stop);
-      stopped = stop;
+    int resume = graph_end;  // first iteration the eager loop below enqueues
+    if (rc != LSK_OK) {
+      // the capture itself failed (nothing of the block was enqueued): clear the
+      // sticky-free launch error and enqueue the blocks instead; a real launch
+      // problem resurfaces there
+      (void)cudaGetLastError();
+      rc = LSK_OK;
+      resume = first_blk;
+    } else {
+      for (int b = 0; b < nblk && rc == LSK_OK && !stopped; ++b) {
+        const cudaError_t e = cudaGraphLaunch(ge[b % nshape], st);
+        if (e != cudaSuccess) rc = sfail(LSK_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+        bool stop = false;
+        if (rc == LSK_OK) rc = poll.after_check(ranks[0].act, st, stop);
+        stopped = stop;
+      }
     }
     destroy();
     S_TRY(rc);
-    for (int k = graph_end; k <= a.max_iter && !stopped; ++k) {
+    if (resume == first_blk)  // eager fallback: the checkpoint counter is not used
+      for (Rank& R : ranks) k_set_int<<<1, 1, 0, st>>>(R.kk, 0);
+    for (int k = resume; k <= a.max_iter && !stopped; ++k) {
       S_TRY(iterate(k));
       if ((k - 1) % c == 0) {
         bool stop = false;
