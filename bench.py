@@ -487,7 +487,8 @@ def run_c4(args, ws, rank, comm, barrier, shard, X, Y, steps):
 
     cfg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=C4_K)
     kw = dict(comm=comm, shard=shard) if comm is not None else {}
-    PT.solve_points_otf(X, Y, None, None, cfg, normalize="max", **kw)  # warm-up
+    for _ in range(max(1, min(args.warmup, 3))):  # warm-up solves
+        PT.solve_points_otf(X, Y, None, None, cfg, normalize="max", **kw)
     barrier()
     torch.cuda.synchronize()
     dev = 0.0
@@ -611,7 +612,7 @@ def sharded_line(args, ws, rank, comm, barrier, local):
            "d2h_bytes_per_step": 2 * C4_N * 4 + 64,
            "path": "paper_2605_00837_b200.solve_points_otf(numpy X, Y, comm=..., shard='partials') -> numpy potentials"}
     return {"metric": METRIC, "value": c4["value"], "unit": "iters/s", "n_gpus": ws, "steps": steps,
-            "warmup": 1, "ms_per_step": c4["ms_per_iter"] * C4_K, "higher_is_better": True, "scaling": "strong",
+            "warmup": max(1, min(args.warmup, 3)), "ms_per_step": c4["ms_per_iter"] * C4_K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (generate_rigid_pair, seed 0)",
             "config": {"workload": c4["workload"], "n": C4_N, "m": C4_N, "eps": 1e-3, "iterations_per_step": C4_K,
                        "parallelism": f"row-sharded x{ws}, column partials allgathered (NCCL)",
@@ -633,6 +634,9 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the other-config rate lines")
     ap.add_argument("--exact", action="store_true", help="exact two-pass variant instead of stale shift")
     ap.add_argument("--direct", action="store_true", help="no multiplicative column update (LSK_FLAG_NO_MULT)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the N > 1 line (C4 through the library's NCCL communicator) even on one rank: "
+                         "a smoke test of the multi-GPU path on a single GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -645,7 +649,11 @@ def main():
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or args.sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(ws))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
@@ -653,11 +661,11 @@ def main():
             dist.barrier()
 
     comm = None
-    if ws > 1:
+    if ws > 1 or args.sharded:
         from paper_2605_00837_b200 import dist as D
 
         comm = D.Communicator.from_torch_distributed()
-    if ws == 1:
+    if ws == 1 and not args.sharded:
         line, X, Y = c2_line(args, local)
         if not args.no_extra:
             line["scaling_configs"] = scaling_configs(args, 1, 0, None, barrier, local)
@@ -672,7 +680,7 @@ def main():
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
-    if ws > 1:
+    if ws > 1 or args.sharded:
         barrier()
         dist.destroy_process_group()
 

@@ -5,11 +5,13 @@ One process per GPU; ``torch.distributed`` is only the bootstrap channel: rank
 existing process group (gloo or nccl), and every rank builds the library's own
 communicator (``lsk_comm_create``) that the solver uses on its CUDA stream.
 
-Sharding rule (owner computes, ``lsk_solve_points_f32``): rank r of P owns rows
-``[r n/P, (r+1) n/P)`` for the f update and columns ``[r m/P, (r+1) m/P)`` for
-the g update; the potentials are allgathered after each half-step. Batched
-independent problems are split across ranks instead (``split_batch``), with no
-communication at all.
+Sharding designs (``lsk_solve_points_f32``, include/lsk.h): column partials
+(default; rank r owns a slab of whole 2048-point chunks of the source cloud,
+the per-column partials of its rows are allgathered and merged by the top of a
+fixed tree), allreduce (the stale sums by ncclAllReduce) and owner computes
+(rank r owns rows ``[r ceil(n/P), ...)`` for f and columns ``[r ceil(m/P), ...)``
+for g, potential slabs allgathered). Batched independent problems are split
+across ranks instead (``split_batch``), with no communication at all.
 """
 
 import ctypes
