@@ -62,7 +62,10 @@ using Solver8k = lsk::DenseSolver<256, 8, 6>;
 using Solver1kU = lsk::DenseSolver<256, 1, 16, true>;
 using Solver2kU = lsk::DenseSolver<256, 2, 16, true>;
 using Solver4kU = lsk::DenseSolver<256, 4, 12, true>;
-using Solver8kU = lsk::DenseSolver<256, 8, 6, true>;
+#ifndef LSK_X_STAGES8U
+#define LSK_X_STAGES8U 6
+#endif
+using Solver8kU = lsk::DenseSolver<256, 8, LSK_X_STAGES8U, true>;
 
 template <class SV>
 __global__ void __launch_bounds__(SV::NW * 32, 1) k_solve_dense(lsk::DenseArgs a) {

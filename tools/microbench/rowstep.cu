@@ -14,7 +14,10 @@
 
 using namespace lsk;
 
-constexpr int NT = 256, V = 8, P2 = 2 * V, W = 4 * V * NT, ROWS = 512;
+#ifndef RS_WARPS
+#define RS_WARPS 8
+#endif
+constexpr int NT = 32 * RS_WARPS, V = 64 / RS_WARPS, P2 = 2 * V, W = 4 * V * NT, ROWS = 512;
 
 template <int TEAMS, bool SYNC, bool FIN, bool GSM>
 __global__ void __launch_bounds__(NT * TEAMS, 1) kern(float* out, unsigned long long* cyc, float negzero) {
@@ -47,8 +50,8 @@ __global__ void __launch_bounds__(NT * TEAMS, 1) kern(float* out, unsigned long 
     const int pb = (k - 1) & 1;
     float S = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; q += 4) {
-      const float4 t = *reinterpret_cast<const float4*>(red + team * 16 + pb * 8 + q);
+    for (int q = 0; q < RS_WARPS; q += 4) {
+      const float4 t = *reinterpret_cast<const float4*>(red + team * 64 + pb * 32 + q);
       S += (t.x + t.y) + (t.z + t.w);
     }
     float fi = fold + 1e-7f * S;
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(NT * TEAMS, 1) kern(float* out, unsigned long 
     float s0, s1;
     up2(s2, s0, s1);
     float s = warp_sum(s0 + s1);
-    if (lane == 0) red[team * 16 + (k & 1) * 8 + w] = s;
+    if (lane == 0) red[team * 64 + (k & 1) * 32 + w] = s;
     fold = fi;
   }
   unsigned long long t1 = clock64();
@@ -91,7 +94,7 @@ void run(const char* name) {
   unsigned long long* cyc;
   cudaMalloc(&out, 148 * 512 * 4);
   cudaMalloc(&cyc, 148 * 8);
-  const int smem = (2 * W + 64) * 4;
+  const int smem = (2 * W + 128) * 4;
   cudaFuncSetAttribute(kern<TEAMS, SYNC, FIN, GSM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int r = 0; r < 2; ++r) kern<TEAMS, SYNC, FIN, GSM><<<148, NT * TEAMS, smem>>>(out, cyc, -0.0f);
   cudaError_t e = cudaDeviceSynchronize();
