@@ -254,17 +254,27 @@ __device__ __forceinline__ typename Op::T leaf_tree(int lo, int cnt, int nreal, 
   int lev[kTreeDepth];
   int sp = 0;
   const int hi = min(lo + cnt, nreal);
-  for (int l = lo; l < hi; ++l) {
-    T v = get(l);
-    int lv = 0;
-    while (sp > 0 && lev[sp - 1] == lv) {
-      v = Op::merge(stk[sp - 1], v);
-      --sp;
-      ++lv;
+  // leaves are loaded 8 at a time (all in flight) and folded in the same order
+  constexpr int PF = 8;
+  for (int l0 = lo; l0 < hi; l0 += PF) {
+    T buf[PF];
+#pragma unroll
+    for (int u = 0; u < PF; ++u) buf[u] = (l0 + u < hi) ? get(l0 + u) : Op::ident();
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      if (l0 + u < hi) {
+        T v = buf[u];
+        int lv = 0;
+        while (sp > 0 && lev[sp - 1] == lv) {
+          v = Op::merge(stk[sp - 1], v);
+          --sp;
+          ++lv;
+        }
+        stk[sp] = v;
+        lev[sp] = lv;
+        ++sp;
+      }
     }
-    stk[sp] = v;
-    lev[sp] = lv;
-    ++sp;
   }
   if (sp == 0) return Op::ident();
   T acc = stk[sp - 1];
