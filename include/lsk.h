@@ -42,7 +42,8 @@ extern "C" {
 #define LSK_FLAG_EXPANSION 8   /* points, eps >= 5e-3: cost as |x|^2+|y|^2-2x.y in the stale sweeps; the
                                   caller requests it only when (max|x-x0|^2 + max|y-x0|^2) 2^-24 /
                                   (eps * normaliser) is small (x0 = the problem's first source point) */
-#define LSK_FLAG_NO_MULT 32    /* dense m <= 8192, uniform nu, n*m >= 2^20, 1e-3 <= eps <= 2e-3: disable the
+#define LSK_FLAG_NO_MULT 32    /* dense m <= 8192, uniform nu, n*m >= 2^20, 1e-3 <= eps <= 2e-3, iterations
+                                  1..1000 of a solve: disable the
                                   multiplicative column update (g-side terms from the f-side ones) */
 #define LSK_FLAG_STD_MULTIKERNEL 64 /* standard domain: force the two-pass multi-kernel loop (fp32 m <= 8192
                                        otherwise runs the one-pass persistent kernel) */

@@ -110,6 +110,7 @@ struct DenseLayout {
   size_t off_f0, off_g0, zero_bytes, off_f1, off_g1, off_part, off_pairs, off_err, off_flag, off_redo, off_errrow, off_cost, total;
 };
 
+constexpr int kMultIters = 1000;       // iterations that may use the multiplicative column update
 constexpr int kClusterMaxRows = 512;  // where the single-cluster solver beats the grid one (profiles/r2_c1_cluster.md)
 
 inline int dense_width(int m) {
@@ -268,6 +269,11 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   // the gate is eps in [1e-3, 2e-3].
   a.mult = (a.stale && eps >= 1e-3 && eps <= 2e-3 && (long long)n * m >= (1LL << 20) && !(flags & LSK_FLAG_NO_MULT))
                ? 1 : 0;
+  // and only for the first kMultIters iterations: the drift is pinned at C2 up
+  // to K = 1000 (6.5e-6 on g); later iterations run the direct arithmetic, so a
+  // long solve (C2 to tolerance 1e-6 takes ~2020) keeps the drift of its first
+  // 1000 instead of accumulating it (tests/test_gpu_parity_long.py)
+  a.mult_iters = kMultIters;
   a.f0 = reinterpret_cast<float*>(ws + L.off_f0);
   a.f1 = reinterpret_cast<float*>(ws + L.off_f1);
   a.g0 = reinterpret_cast<float*>(ws + L.off_g0);

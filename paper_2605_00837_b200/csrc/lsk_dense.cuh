@@ -52,7 +52,8 @@ struct DenseArgs {
   float negzero;  // -0.0f, passed at run time (see muladd_rn2)
   double tol;
   int max_iter, check, stale, want_cost;
-  int mult;       // column update from the f-side terms (see fused_pass_mult)
+  int mult;       // column update from the f-side terms (see fused_pass_mult) ...
+  int mult_iters; // ... for iterations k <= mult_iters only (its drift grows with k)
   // workspace (zero-initialised by the host where noted)
   float* f0; float* f1;  // f^k lives in f[k & 1]; f0 = 0 on entry
   float* g0; float* g1;  // g^k lives in g[k & 1]; g0 = 0 on entry
@@ -1002,7 +1003,7 @@ struct DenseSolver {
       LSK_TR(0);
       if (fused) {
         if (do_check) fused_pass<true>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
-        else if (UNI && a.mult) fused_pass_mult(fb((k - 1) & 1), fb(k & 1));
+        else if (UNI && a.mult && k <= a.mult_iters) fused_pass_mult(fb((k - 1) & 1), fb(k & 1));
         else fused_pass<false>(fb((k - 1) & 1), fb(k & 1), err_acc, bad);
         LSK_TR(1);
         store_stale_partials();

@@ -202,6 +202,12 @@ def long_c2():
     points_case("g2_c2_n8192_k1000", 8192, 2, 0, 1e-3, 1000)
 
 
+def long_c2_k2000():
+    """C2 at 2000 iterations: the multiplicative column update's drift grows with K
+    (profiles/r2_c1_cluster.md); C2 reaches marginal error 1e-6 at ~2020."""
+    points_case("g2_c2_n8192_k2000", 8192, 2, 0, 1e-3, 2000)
+
+
 def long_c2_k200():
     points_case("g2_c2_n8192_k200", 8192, 2, 0, 1e-3, 200)
 

@@ -64,15 +64,16 @@ def check(name, variant, rep, pot, z):
     assert ec <= RTOL, (name, variant, "cost", ec)
 
 
-DENSE = ["g2_c2_n8192_k200", "g2_c2_n8192_k1000", "g3_c3_n8192_k200", "g3_c3_n8192_k1000"]
+DENSE = ["g2_c2_n8192_k200", "g2_c2_n8192_k1000", "g2_c2_n8192_k2000", "g3_c3_n8192_k200", "g3_c3_n8192_k1000"]
 
 
 @pytest.mark.parametrize("mult", [True, False], ids=["mult", "direct"])
 @pytest.mark.parametrize("name", DENSE)
 def test_dense_benchmarked_configs(cuda_ok, name, mult):
-    """C2 (eps=1e-3) and C3 (eps=1e-4) at n = m = 8192, K = 200 and 1000: the
-    headline kernel (multiplicative column update where it applies, i.e. C2)
-    and the direct g-side arithmetic, both against the reference."""
+    """C2 (eps=1e-3) at n = m = 8192, K = 200, 1000 and 2000, and C3 (eps=1e-4) at
+    K = 200 and 1000: the headline kernel (multiplicative column update where it
+    applies -- C2, its first 1000 iterations) and the direct g-side arithmetic,
+    both against the reference."""
     if not have(name):
         pytest.skip(f"fixture {name} not generated")
     z, X, Y, norm = fixture_points(name)
