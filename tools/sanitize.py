@@ -4,10 +4,12 @@ compute-sanitizer (memcheck, racecheck, synccheck, initcheck):
     compute-sanitizer --tool memcheck python tools/sanitize.py
 
 Covers k_solve_dense at all four widths (m <= 1024/2048/4096/8192), general and
-uniform-target instances, the multiplicative column update, the exact
-variant, the m > 8192 loop, k_std_fused (standard domain, fp32 persistent),
-the on-the-fly points kernels (stale, online, cost, consume) and the
-emulated 2-rank column-partials solve. Shapes are small so the tools finish
+uniform-target instances (the single-cluster solver for uniform targets at
+m <= 1024, n <= 512), the multiplicative column update, the exact variant, the
+m > 8192 loop (uniform and general row kernels, fused checkpoint terms),
+k_std_fused (standard domain, fp32 persistent), the on-the-fly points kernels
+(stale, online, cost, consume), their CUDA-graph replay, and the emulated
+2-rank column-partials and owner-computes solves. Shapes are small so the tools finish
 in minutes; each solve still runs several checks and the grid barriers.
 """
 
@@ -49,6 +51,10 @@ def main():
         r, _ = lsk.solve(C, lsk.make_distribution(np.ones(40)), lsk.make_distribution(np.ones(9000)),
                          lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=7, check_interval=3))
         print("dense loop", r.status, flush=True)
+        r, _ = lsk.solve(C, lsk.make_distribution(rng.uniform(0.5, 1.5, 40)),
+                         lsk.make_distribution(rng.uniform(0.5, 1.5, 9000)),
+                         lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=7, check_interval=3))
+        print("dense loop general", r.status, flush=True)
     if only in ("all", "standard"):
         X, Y = rng.uniform(0, 1, (500, 2)), rng.uniform(0, 1, (700, 2))
         C = lsk.squared_euclidean_cost(X, Y)
@@ -65,6 +71,12 @@ def main():
         from paper_2605_00837_b200.applications import barycentric_map_points
 
         barycentric_map_points(X, Y, pot, 1e-3, normalize="max")
+        # CUDA-graph replay of the iteration blocks (>= 3 blocks of check_interval iterations)
+        cfgg = lsk.SinkhornConfig(epsilon=1e-3, tolerance=1e-30, max_iterations=20, check_interval=3)
+        r, _ = PT.solve_points_otf(X, Y, None, None, cfgg, normalize="max")
+        print("points graphs", r.status, r.iterations, flush=True)
+        rb = PT.solve_points_batched(np.stack([X[:300]] * 3), np.stack([Y[:400]] * 3), cfgg)
+        print("points batched graphs", rb[0][0].status, flush=True)
         X2, Y2 = rng.uniform(0, 1, (4100, 3)), rng.uniform(0, 1, (900, 3))
         for shard in ("partials", "owner"):
             r, _, mism = PT.solve_points_emulated(X2, Y2, None, None, cfg, 2, "max", shard=shard)
