@@ -261,15 +261,14 @@ struct ClusterSolver {
   // CTA's err / bad into scal (fixed warp order)
   __device__ void cta_check(float err_acc, int bad) {
     if (lane == 0) sm[kOffS + w] = err_acc;
-    bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) sm[kOffS + kSBad] = bad ? 1.f : 0.f;
+    bad = __syncthreads_or(bad);  // CTA-uniform in every thread
     if (w == 0) {
       float e = 0.f;
       for (int u = 0; u < NW; ++u) e += sm[kOffS + u];
       if (lane < CL) {
         float* rs = remote(sm + kOffS, lane);
         rs[kMErr + crank] = e;
-        rs[kMBad + crank] = sm[kOffS + kSBad];
+        rs[kMBad + crank] = bad ? 1.f : 0.f;
       }
     }
   }
