@@ -882,7 +882,10 @@ struct DenseSolver {
       const int c = t % nc, q = t / nc, j = j0 + c;
       // every partial of the slice in flight at once (one L2 round trip), then
       // summed in a fixed order
-      constexpr int KB = 24;
+#ifndef LSK_X_COMB_KB
+#define LSK_X_COMB_KB 40  // >= G / QS at C2 (148 / 4): every partial of a slice in one L2 round trip
+#endif
+      constexpr int KB = LSK_X_COMB_KB;
       float s = 0.f;
       for (int k0 = q; k0 < G; k0 += KB * QS) {
         float v[KB];
