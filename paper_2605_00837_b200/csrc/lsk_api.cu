@@ -1,5 +1,6 @@
 // C-ABI implementation (include/lsk.h): argument checks, workspace carving,
 // launch configuration. All compute lives in lsk_dense.cuh / lsk_kernels.cuh.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -111,7 +112,11 @@ struct DenseLayout {
 };
 
 constexpr int kMultIters = 1000;       // iterations that may use the multiplicative column update
-constexpr int kClusterMaxRows = 512;  // where the single-cluster solver beats the grid one (profiles/r2_c1_cluster.md)
+#ifndef LSK_X_CLUSTER_MAX_ROWS
+#define LSK_X_CLUSTER_MAX_ROWS 128
+#endif
+constexpr int kClusterMaxRows = LSK_X_CLUSTER_MAX_ROWS;  // one cluster up to one row per warp; more rows: the
+                                                        // multi-cluster solver (profiles/r2_c1_cluster.md)
 
 inline int dense_width(int m) {
   if (m <= 1024) return 1024;
@@ -173,6 +178,49 @@ int32_t launch_cluster(lsk::DenseArgs& a, cudaStream_t st, bool& launched) {
     return LSK_OK;  // not schedulable on this device: the caller falls back
   }
   LSK_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+  launched = true;
+  return LSK_OK;
+}
+
+// m <= 1024, more rows than one cluster's warps: NCL clusters of CL CTAs, just
+// enough for one row per warp (at most what fits on the device at once), one
+// grid barrier per iteration; a cooperative launch, so co-residency of the
+// clusters is guaranteed or the launch is refused (then the caller falls back)
+template <int CL>
+int32_t launch_multicluster(lsk::DenseArgs& a, int G, cudaStream_t st, bool& launched) {
+  using SV = lsk::ClusterSolver<CL, true>;
+  launched = false;
+  auto kern = k_solve_dense<SV>;
+  LSK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SV::kSmemBytes)));
+  if (CL > 8) LSK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(SV::NT);
+  cfg.dynamicSmemBytes = SV::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nmax = 0;
+  if (cudaOccupancyMaxActiveClusters(&nmax, kern, &cfg) != cudaSuccess || nmax < 2) {
+    (void)cudaGetLastError();
+    return LSK_OK;
+  }
+  const int rows_per_cluster = CL * SV::NW;
+  int ncl = std::min({nmax, SV::kMaxClusters, (a.n + rows_per_cluster - 1) / rows_per_cluster, G / 2});
+  if (ncl < 2 || (long long)a.n > (long long)SV::RPC * ncl * CL) return LSK_OK;
+  cfg.gridDim = dim3(ncl * CL);
+  cfg.numAttrs = 2;
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return LSK_OK;
+  }
   launched = true;
   return LSK_OK;
 }
@@ -296,11 +344,20 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   a.trace_iter = trace_iter;
   a.trace_err = trace_err;
   bool done = false;
-  if ((flags & LSK_FLAG_UNIFORM_NU) && L.W == 1024 && n <= kClusterMaxRows && !(flags & LSK_FLAG_NO_CLUSTER)) {
+  if ((flags & LSK_FLAG_UNIFORM_NU) && L.W == 1024 && !(flags & LSK_FLAG_NO_CLUSTER)) {
     lsk::DenseArgs ac = a;
-    ac.mult = 0;  // the cluster solver always runs the reference's direct g-side arithmetic
-    if ((rc = launch_cluster<16>(ac, st, done))) return rc;
-    if (!done && (rc = launch_cluster<8>(ac, st, done))) return rc;
+    ac.mult = 0;  // the cluster solvers always run the reference's direct g-side arithmetic
+    if (n > kClusterMaxRows) {
+#ifdef LSK_X_MC_CL8
+      if ((rc = launch_multicluster<8>(ac, L.G, st, done))) return rc;
+#endif
+      if (!done && (rc = launch_multicluster<16>(ac, L.G, st, done))) return rc;
+      if (!done && (rc = launch_multicluster<8>(ac, L.G, st, done))) return rc;
+    }
+    if (!done && n <= kClusterMaxRows * 4) {
+      if ((rc = launch_cluster<16>(ac, st, done))) return rc;
+      if (!done && (rc = launch_cluster<8>(ac, st, done))) return rc;
+    }
   }
   if (done) {
   } else if (flags & LSK_FLAG_UNIFORM_NU) {

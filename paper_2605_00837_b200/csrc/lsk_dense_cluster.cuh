@@ -30,6 +30,18 @@
 //    over DSMEM in rank order, finishes g_j and stores it into every CTA's
 //    shared g copy (DSMEM) -> barrier.cluster. Two cluster barriers per
 //    iteration; the check's error sum rides on the first.
+// MC = true (multi-cluster): NCL clusters of CL CTAs (up to one CTA per SM)
+// split the rows, so C1 (n = 1024) gives every warp at most one row. Each
+// cluster first combines its CTAs' partials over DSMEM as above; the CTA that
+// owns column slice s stores its cluster's slice sums to global memory, ONE
+// software grid barrier per iteration, then EVERY cluster sums the NCL
+// cluster partials of its slices in cluster order, finishes g and broadcasts
+// it into its CTAs' shared copies -- the same bits in every cluster, so the
+// guard decision and the stop decision need no further exchange. The global
+// slots are double-buffered by iteration parity (every iteration has at least
+// one grid barrier, so a slot is rewritten only after every cluster has read
+// it). This replaces the 148-CTA DenseSolver's two grid barriers and 148-way
+// combine per iteration at m <= 1024 (profiles/r2_c1_cluster.md).
 // Stale shifts and guards are those of DenseSolver: a row sum
 // outside [1e-20, 1e30] is redone exactly in-warp from the registers; a column
 // sum outside the band redoes the iteration's g with the exact online
@@ -41,7 +53,7 @@
 
 namespace lsk {
 
-template <int CL>
+template <int CL, bool MC = false>
 struct ClusterSolver {
   static constexpr bool kUniform = true;
   static constexpr int NT = 256, NW = NT / 32;
@@ -63,11 +75,15 @@ struct ClusterSolver {
   // (DSMEM stores before the barrier), so the reads after it are local
   static constexpr int kMErr = 16, kMBad = 16 + 16, kMGuard = 16 + 32;
   static_assert(CL <= 16, "mailbox width");
+  static constexpr int kMaxClusters = 32;  // MC: cluster partials per column summed with all loads in flight
 
   const DenseArgs& a;
   cooperative_groups::cluster_group cl;
   float* sm;
   int crank, lane, w, r0, r1;
+  int cid, ncl;        // cluster index / count (MC; 0 / 1 otherwise)
+  unsigned epoch = 0;  // MC: software grid barrier epochs
+  int nexact = 0;      // MC: exact column passes so far (their global slots alternate)
   int nrw;       // rows of this warp: r0 + w + NW q, q < nrw
   int q_iss;     // ring: rows issued (in the warp's cyclic row sequence)
   f2 inv2, l2e2, nz2, lnu2;
@@ -79,10 +95,13 @@ struct ClusterSolver {
       : a(args), cl(cooperative_groups::this_cluster()) {
     sm = reinterpret_cast<float*>(smem);
     crank = int(cl.block_rank());
+    cid = MC ? int(blockIdx.x) / CL : 0;
+    ncl = MC ? int(gridDim.x) / CL : 1;
     lane = threadIdx.x & 31;
     w = threadIdx.x >> 5;
-    r0 = int((long long)crank * a.n / CL);
-    r1 = int((long long)(crank + 1) * a.n / CL);
+    const int gi = cid * CL + crank, gn = ncl * CL;
+    r0 = int((long long)gi * a.n / gn);
+    r1 = int((long long)(gi + 1) * a.n / gn);
     nrw = (r1 - r0 - w + NW - 1) / NW;
     if (nrw < 0) nrw = 0;
     q_iss = 0;
@@ -119,6 +138,8 @@ struct ClusterSolver {
       for (int k = 0; k < R - 1; ++k) issue_row();
   }
   // the next row of the sequence into registers; its slot is refilled R-1 rows ahead
+  // (refilling lazily at the next take, so no copy is in flight at a cluster
+  // barrier, measured the same: profiles/r2_c1_cluster.md)
   __device__ __forceinline__ void take_row(f2 (&c)[P2]) {
     asm volatile("cp.async.wait_group %0;" ::"n"(R - 2) : "memory");
     const float* slot = sm + kOffR + (w * R + (q_iss - (R - 1)) % R) * W;
@@ -174,11 +195,26 @@ struct ClusterSolver {
 
   // ---- the f pass of iteration k over this warp's rows (+ the check of iterate
   // k-1 when CHECK; + the column update when FUSED)
+#ifdef LSK_X_TRACE
+  int cur_k = 0;
+// (the value's MOV waits on its scoreboard; a warp issues in order, so the clock
+// read that follows stamps the time the value became available)
+#define LSK_RTR(slot, val)                                                                   \
+  if (threadIdx.x == 0 && blockIdx.x == 0 && cur_k >= 20 && cur_k < 30 && i == r0) {      \
+    float dep_ = (val);                                                                     \
+    asm volatile("mov.b32 %0, %0;" : "+f"(dep_));                                           \
+    lsk_x_trace[(cur_k - 20) * 4 + (slot)] = clock64() + (dep_ == 1.2345e-30f ? 1 : 0);    \
+  }
+#else
+#define LSK_RTR(slot, val)
+#endif
   template <bool FUSED, bool CHECK>
   __device__ void f_pass(const float* fprev, float* fnew, float& err_acc, int& bad) {
     for (int i = r0 + w; i < r1; i += NW) {
       f2 c[P2];
+      LSK_RTR(0, 0.f);
       take_row(c);
+      LSK_RTR(1, __uint_as_float(unsigned(c[0])));
       const float fold = fprev[i - r0], lmu = sm[kOffLm + i - r0];
       float fi;
       f2 e[P2];
@@ -202,6 +238,7 @@ struct ClusterSolver {
           exact_lse<false>(c, 0.f, M, S);
         }
         fi = __fmul_rn(a.neg_eps, lse_finish(M, S));
+        LSK_RTR(2, fi);
       } else {
         float M, S;
         exact_lse<false>(c, 0.f, M, S);
@@ -237,6 +274,7 @@ struct ClusterSolver {
                                              mul2(mul2(g2[p], inv2), l2e2))));
         }
       }
+      LSK_RTR(3, __uint_as_float(unsigned(ac2[P2 - 1])));
     }
   }
 
@@ -273,7 +311,7 @@ struct ClusterSolver {
     }
   }
   // after a cluster barrier: the cluster's err (rank order) and bad, identical in every CTA
-  __device__ bool decide(int kk, bool& failed) {
+  __device__ void cluster_err(float& err, int& bad) const {
     // lane r reads rank r's scalars (all in flight at once); the butterfly sum
     // has the same bits in every lane, warp and CTA
     float er = 0.f;
@@ -282,8 +320,41 @@ struct ClusterSolver {
       er = sm[kOffS + kMErr + lane];
       bd = sm[kOffS + kMBad + lane] != 0.f;
     }
-    const float err = warp_sum(er);
-    const int bad = __any_sync(0xffffffffu, bd);
+    err = warp_sum(er);
+    bad = __any_sync(0xffffffffu, bd);
+  }
+  __device__ bool decide(int kk, bool& failed) {
+    float err;
+    int bad;
+    if constexpr (MC) {
+      // the NCL cluster errors (published before the grid barrier, slot kk + 1 parity), cluster order
+      const int sl = ((kk + 1) & 1) * ncl;
+      float er = 0.f;
+      int bd = 0;
+      if (lane < ncl) {
+        er = ldcg(a.errpart + sl + lane);
+        bd = __ldcg(a.flagpart + sl + lane);
+      }
+      err = warp_sum(er);
+      bad = __any_sync(0xffffffffu, bd != 0);
+    } else {
+      cluster_err(err, bad);
+    }
+    return decide_from(err, bad, kk, failed);
+  }
+  // MC, after the cluster barrier: the cluster's check scalars to global slot (k & 1)
+  __device__ void publish_cluster_err(int k) {
+    if (crank == 0 && w == 0) {
+      float err;
+      int bad;
+      cluster_err(err, bad);
+      if (lane == 0) {
+        a.errpart[(k & 1) * ncl + cid] = err;
+        a.flagpart[(k & 1) * ncl + cid] = bad;
+      }
+    }
+  }
+  __device__ bool decide_from(float err, int bad, int kk, bool& failed) {
     bool stop = false;
     int status = 0;
     float e = err;
@@ -291,7 +362,7 @@ struct ClusterSolver {
     if (bad) { stop = true; status = 2; e = NAN; append = false; }
     else if (!isfinite(err)) { stop = true; status = 2; }
     else if (err < a.tol) { stop = true; status = 1; }
-    if (crank == 0 && threadIdx.x == 0) {
+    if (cid == 0 && crank == 0 && threadIdx.x == 0) {
       if (append) {
         const int t = *a.n_trace;
         a.trace_iter[t] = kk;
@@ -311,6 +382,62 @@ struct ClusterSolver {
   // are spread over every thread.
   static constexpr int NSL = NT / CPC;   // rank slices
   static constexpr int RPS = CL / NSL;   // ranks per slice
+  // sum of the CL CTA partials of this CTA's column slice (thread c < CPC holds column c's)
+  __device__ float cluster_slice_sum() {
+    static_assert(NT % CPC == 0 && CL % (NT / CPC) == 0, "slicing");
+    float* tmp = sm + kOffW;
+    {
+      const int c = threadIdx.x % CPC, sl = threadIdx.x / CPC, j = crank * CPC + c;
+      float v[RPS];
+#pragma unroll
+      for (int u = 0; u < RPS; ++u) v[u] = remote(sm + kOffC, sl * RPS + u)[j];
+      float S = 0.f;
+#pragma unroll
+      for (int u = 0; u < RPS; ++u) S += v[u];
+      tmp[sl * CPC + c] = S;
+    }
+    __syncthreads();
+    float S = 0.f;
+    if (threadIdx.x < CPC) {
+#pragma unroll
+      for (int sl = 0; sl < NSL; ++sl) S += tmp[sl * CPC + threadIdx.x];
+    }
+    return S;
+  }
+  // MC: the software grid barrier, every CTA arriving (one arrival per cluster
+  // behind a cluster barrier measured slower: the extra barrier.cluster costs
+  // more than the 16x fewer same-address atomics, profiles/r2_c1_cluster.md)
+  __device__ void mc_barrier() { grid_barrier(a.bar, epoch); }
+  // MC stage 1 (before the grid barrier): the cluster's slice sums to global slot (k & 1)
+  __device__ void stale_publish(int k) {
+    const float S = cluster_slice_sum();
+    if (threadIdx.x < CPC) a.part[(size_t)((k & 1) * ncl + cid) * W + crank * CPC + threadIdx.x] = S;
+  }
+  // MC stage 2 (after it): g^k of the slice from the NCL cluster sums in cluster
+  // order (identical in every cluster), broadcast into the cluster's copies
+  __device__ bool stale_finish(int k) {
+    float* gt = sm + kOffW + NSL * CPC;
+    bool fired = false;
+    if (threadIdx.x < CPC) {
+      const int c = threadIdx.x, j = crank * CPC + c;
+      const float* P = a.part + (size_t)((k & 1) * ncl) * W + j;
+      float v[kMaxClusters];
+#pragma unroll
+      for (int q = 0; q < kMaxClusters; ++q) v[q] = q < ncl ? ldcg(P + (size_t)q * W) : 0.f;
+      float S = 0.f;
+#pragma unroll
+      for (int q = 0; q < kMaxClusters; ++q)
+        if (q < ncl) S += v[q];
+      const float gold = sm[kOffG + j];
+      float gn = __fmul_rn(a.neg_eps, lse_finish(__fmul_rn(-gold, a.inv_eps), S));
+      if (j >= a.m) gn = -INFINITY;
+      else if (!shift_ok(S)) fired = true;
+      gt[c] = gn;
+    }
+    fired = __syncthreads_or(fired);
+    broadcast_g(gt);
+    return fired;
+  }
   __device__ bool combine_stale() {
     static_assert(NT % CPC == 0 && CL % (NT / CPC) == 0, "slicing");
     float* tmp = sm + kOffW;  // [NSL][CPC] slice sums, then [CPC] g (wred is free here)
@@ -405,11 +532,41 @@ struct ClusterSolver {
     }
     __syncthreads();
     float* gt = sm + kOffW + 2 * NSL * CPC;
+    if constexpr (MC) {  // the cluster's pairs -> global slot, grid barrier, NCL pairs merged in cluster order
+      float2* P = a.pairs + (size_t)((nexact & 1) * ncl) * W;
+      if (threadIdx.x < CPC) {
+        const int c = threadIdx.x;
+        float m0 = -INFINITY, s0 = 0.f;
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) pair_merge(m0, s0, tmp[sl * CPC + c].x, tmp[sl * CPC + c].y);
+        P[(size_t)cid * W + crank * CPC + c] = make_float2(m0, s0);
+      }
+      mc_barrier();
+      if (threadIdx.x < CPC) {
+        const int j = crank * CPC + threadIdx.x;
+        float2 v[kMaxClusters];
+#pragma unroll
+        for (int q = 0; q < kMaxClusters; ++q) v[q] = q < ncl ? __ldcg(P + (size_t)q * W + j) : make_float2(-INFINITY, 0.f);
+        float m0 = -INFINITY, s0 = 0.f;
+#pragma unroll
+        for (int q = 0; q < kMaxClusters; ++q)
+          if (q < ncl) pair_merge(m0, s0, v[q].x, v[q].y);
+        tmp[threadIdx.x] = make_float2(m0, s0);
+      }
+      ++nexact;
+    }
     if (threadIdx.x < CPC) {
       const int c = threadIdx.x, j = crank * CPC + c;
-      float m0 = -INFINITY, s0 = 0.f;
+      float m0, s0;
+      if constexpr (MC) {
+        m0 = tmp[c].x;
+        s0 = tmp[c].y;
+      } else {
+        m0 = -INFINITY;
+        s0 = 0.f;
 #pragma unroll
-      for (int sl = 0; sl < NSL; ++sl) pair_merge(m0, s0, tmp[sl * CPC + c].x, tmp[sl * CPC + c].y);
+        for (int sl = 0; sl < NSL; ++sl) pair_merge(m0, s0, tmp[sl * CPC + c].x, tmp[sl * CPC + c].y);
+      }
       float gn = __fmul_rn(a.neg_eps, lse_finish(m0, s0));
       if (j >= a.m) gn = -INFINITY;
       gt[c] = gn;
@@ -477,6 +634,17 @@ struct ClusterSolver {
     int final_k = a.max_iter;
     bool stopped = false, failed = false;
     for (int k = 1; k <= a.max_iter; ++k) {
+#ifdef LSK_X_TRACE
+#define LSK_CTR(slot)                                                                                     \
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && k >= 20 && k < 30)         \
+  lsk_x_trace[1536 + (blockIdx.x == 0 ? 0 : 80) + (k - 20) * 8 + (slot)] = clock64()
+#else
+#define LSK_CTR(slot)
+#endif
+      LSK_CTR(0);
+#ifdef LSK_X_TRACE
+      cur_k = k;
+#endif
       const bool do_check = (k > 1) && ((k - 1) % a.check == 0);
       const bool fused = a.stale && k > 1;
       const bool gbad = load_columns();
@@ -487,24 +655,40 @@ struct ClusterSolver {
       if (fused) {
         if (do_check) f_pass<true, true>(fp, fn, err_acc, bad);
         else f_pass<true, false>(fp, fn, err_acc, bad);
+        LSK_CTR(1);
         cta_partial();
       } else {
         if (do_check) f_pass<false, true>(fp, fn, err_acc, bad);
         else f_pass<false, false>(fp, fn, err_acc, bad);
       }
       if (do_check) cta_check(err_acc, bad);
+      LSK_CTR(2);
       cl.sync();  // (A) CTA partials, check scalars and f^k visible cluster-wide
+      LSK_CTR(3);
+      if constexpr (MC) {  // cluster slice sums and check scalars to global memory, one grid barrier
+        if (fused) stale_publish(k);
+        if (do_check) publish_cluster_err(k);
+        LSK_CTR(4);
+        if (fused || do_check) mc_barrier();
+        LSK_CTR(5);
+      }
       if (do_check && decide(k - 1, failed)) { stopped = true; final_k = k - 1; break; }
       bool need_exact = !fused;
       if (fused) {
-        const bool fired = combine_stale();
+        bool fired;
+        if constexpr (MC) fired = stale_finish(k);
+        else fired = combine_stale();
+        LSK_CTR(6);
         if (w == 0 && lane < CL) remote(sm + kOffS, lane)[kMGuard + crank] = fired ? 1.f : 0.f;
         cl.sync();  // (B) g^k in every CTA's copy; guard flags in every CTA's mailbox
+        LSK_CTR(7);
         need_exact = __any_sync(0xffffffffu, lane < CL && sm[kOffS + kMGuard + lane] != 0.f);
       }
       if (need_exact) {
-        if (crank == 0 && threadIdx.x == 0 && fused) atomicAdd(a.stats + 1, 1);
-        if (fused && crank == 0 && threadIdx.x == 0) atomicMax(a.guard, k);
+        if (cid == 0 && crank == 0 && threadIdx.x == 0 && fused) {
+          atomicAdd(a.stats + 1, 1);
+          atomicMax(a.guard, k);
+        }
         col_exact(fn);
       }
     }
@@ -516,6 +700,10 @@ struct ClusterSolver {
       check_only(fs(final_k), err_acc, bad);
       cta_check(err_acc, bad);
       cl.sync();
+      if constexpr (MC) {
+        publish_cluster_err(final_k + 1);
+        mc_barrier();
+      }
       decide(final_k, failed);
     }
     const int fbuf = final_k & 1;
@@ -533,21 +721,26 @@ struct ClusterSolver {
         sm[kOffS + kSCost] = s;
       }
       cl.sync();
-      if (crank == 0 && w == 0) {
-        float cost = warp_sum(lane < CL ? remote(sm + kOffS, lane)[kSCost] : 0.f);
-        if (lane == 0) {
-          if (!isfinite(cost)) { *a.out_status = 2; cost = NAN; }
-          *a.out_cost = cost;
-        }
+      float cost = 0.f;
+      if (crank == 0 && w == 0) cost = warp_sum(lane < CL ? remote(sm + kOffS, lane)[kSCost] : 0.f);
+      if constexpr (MC) {  // cluster costs -> global, summed in cluster order by cluster 0
+        if (crank == 0 && threadIdx.x == 0) a.costpart[cid] = cost;
+        mc_barrier();
+        if (cid == 0 && crank == 0 && w == 0) cost = warp_sum(lane < ncl ? ldcg(a.costpart + lane) : 0.f);
       }
-    } else if (crank == 0 && threadIdx.x == 0) {
+      if (cid == 0 && crank == 0 && threadIdx.x == 0) {
+        if (!isfinite(cost)) { *a.out_status = 2; cost = NAN; }
+        *a.out_cost = cost;
+      }
+    } else if (cid == 0 && crank == 0 && threadIdx.x == 0) {
       *a.out_cost = NAN;
     }
     // the returned iterate's potentials to global (f of the CTA's rows; g of its columns)
     for (int t = threadIdx.x; t < r1 - r0; t += NT) fb(fbuf)[r0 + t] = fs(final_k)[t];
-    for (int t = threadIdx.x; t < CPC; t += NT)
-      if (crank * CPC + t < a.m) gb(fbuf)[crank * CPC + t] = sm[kOffG + crank * CPC + t];
-    if (crank == 0 && threadIdx.x == 0) {
+    if (cid == 0)
+      for (int t = threadIdx.x; t < CPC; t += NT)
+        if (crank * CPC + t < a.m) gb(fbuf)[crank * CPC + t] = sm[kOffG + crank * CPC + t];
+    if (cid == 0 && crank == 0 && threadIdx.x == 0) {
       *a.out_iters = final_k;
       *a.out_fbuf = fbuf;
     }

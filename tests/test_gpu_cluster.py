@@ -1,7 +1,10 @@
-"""The single-cluster dense solver (csrc/lsk_dense_cluster.cuh): uniform
-targets, m <= 1024, n <= 512 run as ONE 16-CTA thread-block cluster with
-DSMEM exchanges instead of the 148-CTA grid solver (the reference golden
-fixtures of that size in test_gpu_parity.py also run through it).
+"""The cluster dense solvers (csrc/lsk_dense_cluster.cuh), uniform targets,
+m <= 1024: n <= 128 runs as ONE 16-CTA thread-block cluster with DSMEM
+exchanges; 128 < n <= 16384 as the multi-cluster solver (8 clusters of 16
+CTAs on a B200, DSMEM inside a cluster, one software grid barrier per
+iteration between them) -- both instead of the 148-CTA grid solver (the
+reference golden fixtures of those sizes in test_gpu_parity.py, C1 among
+them, also run through them).
 
 Checked against the oracle run live, against the grid solver on awkward
 shapes (one row, empty CTAs and warps, padded columns, the guard paths at
@@ -39,8 +42,8 @@ def launch(C, mu, nu, cfg, *, cluster, mult=True, stale=True):
 
 def test_c1_fixture(cuda_ok):
     """C1 (n=m=1024, eps=1e-2, K=200) against the reference's own output through
-    the default path (the grid kernel; eps = 1e-2 is outside the multiplicative
-    update's gate, so the g-side arithmetic is the reference's)."""
+    the default path (the multi-cluster solver, the reference's direct g-side
+    arithmetic)."""
     z = golden("g1_c1_n1024")
     X, Y = O.uniform_points(1024, 2, 0)
     C = lsk.squared_euclidean_cost(X, Y)
@@ -53,10 +56,10 @@ def test_c1_fixture(cuda_ok):
     assert abs(r["cost"] - float(z["cost"])) <= RTOL * abs(float(z["cost"]))
 
 
-@pytest.mark.parametrize("n", [512, 1024])
+@pytest.mark.parametrize("n", [128, 512, 1024])
 def test_vs_oracle_k300(cuda_ok, n):
     """n x 1024 at eps=1e-2, K=300 against the oracle (the reference's arithmetic):
-    n = 512 through the cluster kernel, n = 1024 through the grid kernel."""
+    n = 128 through the single cluster, 512 and 1024 (C1) through the multi-cluster solver."""
     rng = np.random.default_rng(5)
     X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (1024, 2))
     C64 = O.sq_euclidean_cost(X, Y)
@@ -85,8 +88,10 @@ def test_multiplicative_gate(cuda_ok):
     np.testing.assert_array_equal(a["g"], b["g"])
 
 
-SHAPES = [(1, 1024, 1e-2), (15, 1000, 1e-2), (16, 5, 5e-2), (17, 129, 1e-2), (300, 1021, 1e-3), (512, 1024, 1e-3),
-          (500, 640, 1e-4), (512, 1024, 2e-4)]
+SHAPES = [(1, 1024, 1e-2), (15, 1000, 1e-2), (16, 5, 5e-2), (17, 129, 1e-2), (128, 1024, 1e-3),
+          # multi-cluster: 2 clusters, one row per warp, several rows per warp, padded columns, guards
+          (129, 1024, 1e-2), (300, 1021, 1e-3), (512, 1024, 1e-3), (500, 640, 1e-4), (512, 1024, 2e-4),
+          (1000, 1000, 1e-2), (2048, 1024, 1e-3), (3001, 777, 1e-4), (16000, 512, 1e-2)]
 
 
 @pytest.mark.parametrize("n,m,eps", SHAPES)
@@ -108,12 +113,13 @@ def test_cluster_vs_grid_shapes(cuda_ok, n, m, eps):
     assert abs(a["cost"] - b["cost"]) <= RTOL * abs(b["cost"])
 
 
-def test_cluster_exact_variant_and_early_stop(cuda_ok):
+@pytest.mark.parametrize("n", [100, 512, 2500])
+def test_cluster_exact_variant_and_early_stop(cuda_ok, n):
     """stale_shift=False (exact two-pass rows + the exact column pass every
     iteration) and a tolerance met mid-run: same stop iteration, trace and
     potentials of the returned iterate as the grid solver."""
     rng = np.random.default_rng(3)
-    n, m = 512, 768
+    m = 768
     X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
     C = lsk.squared_euclidean_cost(X, Y)
     mu, nu = lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(m))
@@ -130,12 +136,13 @@ def test_cluster_bitwise_repeats(cuda_ok):
     """Fixed-order reductions: repeated solves are bit-identical (reference
     tests/test_solver.py:247-257)."""
     rng = np.random.default_rng(9)
-    X, Y = rng.uniform(0, 1, (500, 2)), rng.uniform(0, 1, (1000, 2))
-    C = lsk.squared_euclidean_cost(X, Y)
-    mu, w = lsk.make_distribution(np.ones(500)), lsk.make_distribution(np.ones(1000))
-    cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=50)
-    a = launch(C, mu, w, cfg, cluster=True)
-    b = launch(C, mu, w, cfg, cluster=True)
-    np.testing.assert_array_equal(a["f"], b["f"])
-    np.testing.assert_array_equal(a["g"], b["g"])
-    assert a["cost"] == b["cost"] and a["trace"] == b["trace"]
+    for n in (100, 500, 3000):
+        X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (1000, 2))
+        C = lsk.squared_euclidean_cost(X, Y)
+        mu, w = lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(1000))
+        cfg = lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=50)
+        a = launch(C, mu, w, cfg, cluster=True)
+        b = launch(C, mu, w, cfg, cluster=True)
+        np.testing.assert_array_equal(a["f"], b["f"])
+        np.testing.assert_array_equal(a["g"], b["g"])
+        assert a["cost"] == b["cost"] and a["trace"] == b["trace"]
