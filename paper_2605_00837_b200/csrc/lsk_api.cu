@@ -151,6 +151,16 @@ DenseLayout dense_layout(int n, int m) {
   return L;
 }
 
+// LSK_VERBOSE=1: name the dense solver each solve launched (stderr), so tests and
+// sanitizer runs can tell which kernel ran
+bool verbose() {
+  static const bool v = [] {
+    const char* e = getenv("LSK_VERBOSE");
+    return e && *e && *e != '0';
+  }();
+  return v;
+}
+
 // small problems (m <= 1024, uniform targets): one cluster of 16 CTAs (8 where
 // a 16-CTA cluster cannot be scheduled), DSMEM exchanges, no grid barrier
 template <int CL>
@@ -179,6 +189,7 @@ int32_t launch_cluster(lsk::DenseArgs& a, cudaStream_t st, bool& launched) {
   }
   LSK_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   launched = true;
+  if (verbose()) fprintf(stderr, "lsk: dense solver: single cluster of %d CTAs\n", CL);
   return LSK_OK;
 }
 
@@ -222,6 +233,7 @@ int32_t launch_multicluster(lsk::DenseArgs& a, int G, cudaStream_t st, bool& lau
     return LSK_OK;
   }
   launched = true;
+  if (verbose()) fprintf(stderr, "lsk: dense solver: %d clusters of %d CTAs\n", ncl, CL);
   return LSK_OK;
 }
 
@@ -236,6 +248,7 @@ int32_t launch_dense(lsk::DenseArgs& a, int G, cudaStream_t st) {
   void* args[] = {&a};
   LSK_CUDA(cudaLaunchCooperativeKernel((const void*)k_solve_dense<SV>, dim3(G), dim3(SV::NW * 32), args,
                                        SV::kSmemBytes, st));
+  if (verbose()) fprintf(stderr, "lsk: dense solver: grid of %d CTAs, row width %d\n", G, SV::W);
   return LSK_OK;
 }
 

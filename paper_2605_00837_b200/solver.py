@@ -204,7 +204,7 @@ def _report_from(r, t0, return_device=False):
     return report, DualPotentials(alpha=alpha, beta=beta)
 
 
-def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multiplicative=True):
+def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multiplicative=True, cluster=True):
     """Log-domain Sinkhorn from zero potentials (reference solver.py:230-337).
 
     Alternates f (alpha) and g (beta) updates, checks the L1 row-marginal
@@ -218,6 +218,8 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multip
     ``multiplicative=False`` disables the multiplicative column update of the
     uniform-target kernel (``LSK_FLAG_NO_MULT``) and forms every
     g-side argument from the cost element as the reference does.
+    ``cluster=False`` runs the 148-CTA grid solver instead of the cluster
+    solvers at m <= 1024 with uniform targets (``LSK_FLAG_NO_CLUSTER``; A/B).
     ``stale_shift=False`` selects the exact two-pass variant (max pass per
     row, exact column pass every iteration) instead of the one-pass
     stale-shift fast path; ``return_device=True`` leaves the potentials as
@@ -236,7 +238,7 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multip
     log_nu = _dev_f32(torch, nu.log_weights)
     mu32 = _dev_f32(torch, mu.weights)
     r, _ = _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=stale_shift,
-                         uniform_nu=_uniform(nu.log_weights), mult=multiplicative)
+                         uniform_nu=_uniform(nu.log_weights), mult=multiplicative, cluster=cluster)
     return _report_from(r, t0, return_device)
 
 

@@ -1,7 +1,7 @@
 """The cluster dense solvers (csrc/lsk_dense_cluster.cuh), uniform targets,
 m <= 1024: n <= 128 runs as ONE 16-CTA thread-block cluster with DSMEM
-exchanges; 128 < n <= 16384 as the multi-cluster solver (8 clusters of 16
-CTAs on a B200, DSMEM inside a cluster, one software grid barrier per
+exchanges; 128 < n <= 14336 as the multi-cluster solver (up to 7 clusters of
+16 CTAs on a B200, DSMEM inside a cluster, one software grid barrier per
 iteration between them) -- both instead of the 148-CTA grid solver (the
 reference golden fixtures of those sizes in test_gpu_parity.py, C1 among
 them, also run through them).
@@ -91,7 +91,7 @@ def test_multiplicative_gate(cuda_ok):
 SHAPES = [(1, 1024, 1e-2), (15, 1000, 1e-2), (16, 5, 5e-2), (17, 129, 1e-2), (128, 1024, 1e-3),
           # multi-cluster: 2 clusters, one row per warp, several rows per warp, padded columns, guards
           (129, 1024, 1e-2), (300, 1021, 1e-3), (512, 1024, 1e-3), (500, 640, 1e-4), (512, 1024, 2e-4),
-          (1000, 1000, 1e-2), (2048, 1024, 1e-3), (3001, 777, 1e-4), (16000, 512, 1e-2)]
+          (1000, 1000, 1e-2), (2048, 1024, 1e-3), (3001, 777, 1e-4), (14000, 512, 1e-2)]
 
 
 @pytest.mark.parametrize("n,m,eps", SHAPES)
@@ -146,3 +146,30 @@ def test_cluster_bitwise_repeats(cuda_ok):
         np.testing.assert_array_equal(a["f"], b["f"])
         np.testing.assert_array_equal(a["g"], b["g"])
         assert a["cost"] == b["cost"] and a["trace"] == b["trace"]
+
+
+def test_solver_selection(cuda_ok):
+    """Which dense solver runs (LSK_VERBOSE=1 names it on stderr): the single
+    cluster up to 128 rows, the multi-cluster solver for C1, the grid solver
+    with LSK_FLAG_NO_CLUSTER and beyond m = 1024."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_2605_00837_b200 as lsk\n"
+        "rng = np.random.default_rng(0)\n"
+        "for n, m, cl in ((100, 1024, True), (1024, 1024, True), (1024, 1024, False), (300, 2048, True)):\n"
+        "    C = lsk.squared_euclidean_cost(rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2)))\n"
+        "    lsk.solve(C, lsk.make_distribution(np.ones(n)), lsk.make_distribution(np.ones(m)),\n"
+        "              lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=5), cluster=cl)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=dict(os.environ, LSK_VERBOSE="1"),
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    lines = [ln for ln in out.stderr.splitlines() if ln.startswith("lsk: dense solver")]
+    assert len(lines) == 4, out.stderr
+    assert "single cluster" in lines[0]
+    assert "clusters of" in lines[1]
+    assert "grid of" in lines[2] and "width 1024" in lines[2]
+    assert "grid of" in lines[3] and "width 2048" in lines[3]

@@ -4,8 +4,8 @@ compute-sanitizer (memcheck, racecheck, synccheck, initcheck):
     compute-sanitizer --tool memcheck python tools/sanitize.py
 
 Covers k_solve_dense at all four widths (m <= 1024/2048/4096/8192), general and
-uniform-target instances (the single-cluster solver for uniform targets at
-m <= 1024, n <= 512), the multiplicative column update, the exact variant, the
+uniform-target instances (the cluster solvers for uniform targets at m <= 1024:
+single cluster n <= 128, multi-cluster above -- also alone with `cluster`), the multiplicative column update, the exact variant, the
 m > 8192 loop (uniform and general row kernels, fused checkpoint terms),
 k_std_fused (standard domain, fp32 persistent), the on-the-fly points kernels
 (stale, online, cost, consume), their CUDA-graph replay, and the emulated
@@ -55,6 +55,20 @@ def main():
                          lsk.make_distribution(rng.uniform(0.5, 1.5, 9000)),
                          lsk.SinkhornConfig(epsilon=1e-2, tolerance=1e-30, max_iterations=7, check_interval=3))
         print("dense loop general", r.status, flush=True)
+    if only in ("all", "dense", "cluster"):
+        # cluster solvers: single cluster, multi-cluster with one and with several rows per warp,
+        # padded columns, the guards (eps = 1e-4), early stop, exact variant
+        for n, m, eps in ((100, 1000, 1e-2), (300, 1000, 1e-3), (1500, 1024, 1e-2), (700, 900, 1e-4)):
+            X, Y = rng.uniform(0, 1, (n, 2)), rng.uniform(0, 1, (m, 2))
+            C = lsk.squared_euclidean_cost(X, Y)
+            mu, nu = lsk.make_distribution(rng.uniform(0.5, 1.5, n)), lsk.make_distribution(np.ones(m))
+            for stale in (True, False):
+                cfg = lsk.SinkhornConfig(epsilon=eps, tolerance=1e-30, max_iterations=12, check_interval=5)
+                r, _ = lsk.solve(C, mu, nu, cfg, stale_shift=stale)
+                print("cluster", n, m, stale, r.status, r.iterations, flush=True)
+            r, _ = lsk.solve(C, mu, nu, lsk.SinkhornConfig(epsilon=0.05, tolerance=1e-3, max_iterations=300,
+                                                           check_interval=2))
+            print("cluster early stop", n, r.status, r.iterations, flush=True)
     if only in ("all", "standard"):
         X, Y = rng.uniform(0, 1, (500, 2)), rng.uniform(0, 1, (700, 2))
         C = lsk.squared_euclidean_cost(X, Y)
