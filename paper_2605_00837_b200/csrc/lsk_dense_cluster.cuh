@@ -86,6 +86,7 @@ struct ClusterSolver {
   int nexact = 0;      // MC: exact column passes so far (their global slots alternate)
   int nrw;       // rows of this warp: r0 + w + NW q, q < nrw
   int q_iss;     // ring: rows issued (in the warp's cyclic row sequence)
+  int q_row;     // ... = q_iss mod nrw, kept incrementally (no integer division per row)
   f2 inv2, l2e2, nz2, lnu2;
   float bcol;
   f2 g2[P2];   // g^{k-1} of the lane's columns
@@ -105,6 +106,7 @@ struct ClusterSolver {
     nrw = (r1 - r0 - w + NW - 1) / NW;
     if (nrw < 0) nrw = 0;
     q_iss = 0;
+    q_row = 0;
     inv2 = pk2(a.inv_eps, a.inv_eps);
     l2e2 = pk2(kLog2e, kLog2e);
     nz2 = pk2(a.negzero, a.negzero);
@@ -118,9 +120,9 @@ struct ClusterSolver {
 
   // ---- the warp's row ring: row q of the cyclic sequence r0 + w + NW (q mod nrw)
   __device__ __forceinline__ void issue_row() {
-    const int i = r0 + w + NW * (q_iss % nrw);
+    const int i = r0 + w + NW * q_row;
     const float* base = a.C + (long long)i * a.ldc;
-    float* slot = sm + kOffR + (w * R + q_iss % R) * W;
+    float* slot = sm + kOffR + (w * R + (unsigned(q_iss) % R)) * W;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
       const int j0 = col(v);
@@ -129,6 +131,7 @@ struct ClusterSolver {
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     ++q_iss;
+    if (++q_row == nrw) q_row = 0;
   }
   __device__ void ring_init() {
     float4* r4 = reinterpret_cast<float4*>(sm + kOffR + w * R * W);  // columns >= m read as 0
@@ -142,13 +145,14 @@ struct ClusterSolver {
   // barrier, measured the same: profiles/r2_c1_cluster.md)
   __device__ __forceinline__ void take_row(f2 (&c)[P2]) {
     asm volatile("cp.async.wait_group %0;" ::"n"(R - 2) : "memory");
-    const float* slot = sm + kOffR + (w * R + (q_iss - (R - 1)) % R) * W;
+    const float* slot = sm + kOffR + (w * R + (unsigned(q_iss - (R - 1)) % R)) * W;
 #pragma unroll
     for (int v = 0; v < V; ++v) lds2x2(slot + col(v), c[2 * v], c[2 * v + 1]);
     issue_row();
   }
 
   // g^{k-1} from the CTA's shared copy; true if a loaded g (j < m) is non-finite
+  template <bool CHK = true>
   __device__ bool load_columns() {
     bool bad = false;
     const float* gS = sm + kOffG;
@@ -158,7 +162,7 @@ struct ClusterSolver {
       const float tt[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (col(v) + q < a.m) bad |= !isfinite(tt[q]);
+        if (CHK && col(v) + q < a.m) bad |= !isfinite(tt[q]);
       g2[2 * v] = pk2(t.x, t.y);
       g2[2 * v + 1] = pk2(t.z, t.w);
       ac2[2 * v] = 0ull;
@@ -633,6 +637,7 @@ struct ClusterSolver {
     cl.sync();
     int final_k = a.max_iter;
     bool stopped = false, failed = false;
+    int to_check = a.check;  // decremented from k = 2 on: zero at k = check + 1, 2 check + 1, ...
     for (int k = 1; k <= a.max_iter; ++k) {
 #ifdef LSK_X_TRACE
 #define LSK_CTR(slot)                                                                                     \
@@ -645,9 +650,11 @@ struct ClusterSolver {
 #ifdef LSK_X_TRACE
       cur_k = k;
 #endif
-      const bool do_check = (k > 1) && ((k - 1) % a.check == 0);
+      // check of iterate k-1 when (k - 1) % check == 0, k > 1: a countdown, no division
+      const bool do_check = (k > 1) && (--to_check == 0);
+      if (do_check) to_check = a.check;
       const bool fused = a.stale && k > 1;
-      const bool gbad = load_columns();
+      const bool gbad = do_check ? load_columns<true>() : load_columns<false>();
       float err_acc = 0.f;
       int bad = (do_check && gbad) ? 1 : 0;
       const float* fp = fs(k - 1);
