@@ -1,5 +1,3 @@
-export LSK_AB="paper_2605_00837_b200/liblsk.so"
-export LSK_AB_ARGS="--n_128_--m_1024_--eps_1e-2 --n_512_--m_1024_--eps_1e-2 --n_1024_--eps_1e-2 --n_4096_--m_1024_--eps_1e-2"
+export LSK_AB="paper_2605_00837_b200/liblsk.so build/liblsk_chkdirect.so"
+export LSK_AB_ARGS="--n_8192_--eps_1e-3 --n_8192_--eps_1e-3_--check_1000 --n_4096_--m_8192_--eps_1e-3"
 bash tools/gpu_ab.sh
-LSK_LIB=$PWD/build/liblsk_trace.so python tools/trace_cluster.py 1024 1024 | tail -2
-timeout 900 python -m pytest tests/test_gpu_cluster.py tests/test_gpu_parity.py -q -x -p no:cacheprovider 2>&1 | tail -3
