@@ -230,7 +230,7 @@ def other_configs():
     sm, mhz = 148, 1965.0
     mufu_pairs = 16 * sm * mhz * 1e6  # one ex2 per pair evaluation
 
-    def dense(n, eps, K, seed=0, tol=1e-30, reps=2, mult=True):
+    def dense(n, eps, K, seed=0, tol=1e-30, reps=2, mult=False):
         rng = np.random.Generator(np.random.PCG64(seed))
         X = rng.uniform(0.0, 1.0, (n, 2))
         Y = rng.uniform(0.0, 1.0, (n, 2))
@@ -261,9 +261,11 @@ def other_configs():
                 break
         return out
 
-    v, _ = dense(8192, 1e-3, 1000, mult=False)
-    out["C2_direct"] = {"workload": "C2 with the direct g-side arithmetic (LSK_FLAG_NO_MULT): every argument "
-                                    "rounded exactly as the reference", "iters_per_s": v}
+    v, _ = dense(8192, 1e-3, 1000, mult=True)
+    out["C2_mult_opt_in"] = {"workload": "C2 with the OPT-IN multiplicative column update (LSK_FLAG_MULT): an "
+                                         "approximation, not the headline -- its potentials drift from the "
+                                         "reference's by up to ~3e-5 at K=1000 (profiles/r2_mult_drift.md)",
+                             "iters_per_s": v}
     v, _ = dense(1024, 1e-2, 200)
     out["C1"] = {"workload": "dense n=m=1024 2-D points, eps=1e-2, 200 iterations", "iters_per_s": v,
                  "ms_per_solve": 200 / v * 1e3}
@@ -356,7 +358,7 @@ def c2_line(args, clocks_index):
     wsbuf = None
     for _ in range(args.warmup):
         r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf,
-                                   uniform_nu=True, mult=not args.direct)
+                                   uniform_nu=True, mult=args.mult)
     torch.cuda.synchronize()
     res = r.res.cpu().numpy()
     assert int(res[1]) == K, res
@@ -368,7 +370,7 @@ def c2_line(args, clocks_index):
         e0.record()
         for _ in range(args.steps):
             r, wsbuf = S._launch_solve(torch, C, log_mu, log_mu, mu32, cfg, stale=not args.exact, ws=wsbuf,
-                                       uniform_nu=True, mult=not args.direct)
+                                       uniform_nu=True, mult=args.mult)
             evs.append((r.ev0, r.ev1))
         e1.record()
         torch.cuda.synchronize()
@@ -385,11 +387,11 @@ def c2_line(args, clocks_index):
     del Xd, Yd
     host_cost = lsk.CostMatrix(values=C64)
     e2e_steps = max(3, args.steps)
-    lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=not args.direct)
+    lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=args.mult)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        rep, pot = lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=not args.direct)
+        rep, pot = lsk.solve(host_cost, w, w, cfg, stale_shift=not args.exact, multiplicative=args.mult)
     torch.cuda.synchronize()
     t_e2e = time.perf_counter() - t0
     # bytes over PCIe: the fp64 host matrix is rounded to fp32 on the host cores (solver.py:253
@@ -407,7 +409,7 @@ def c2_line(args, clocks_index):
     onepass = N * N * 4 * K      # compulsory bytes of the fused single pass (C read once per iteration)
     ach = twopass / t_kern / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r1_dense_ncu_traffic.json")
+    prof = os.path.join(ROOT, "profiles", "r2_dense_ncu_traffic.json")
     if os.path.exists(prof):
         try:
             traffic = json.load(open(prof))["dram_bytes_per_iteration"] * K
@@ -429,9 +431,9 @@ def c2_line(args, clocks_index):
                                    f"{K} iterations/step, check every {CHECK}, transport cost",
                        "n": N, "m": N, "eps": EPS, "iterations_per_step": K,
                        "variant": ("exact-two-pass" if args.exact else "stale-shift one-pass")
-                       + (", direct g-side arithmetic" if args.direct else
-                          ", multiplicative column update (uniform targets; parity vs the reference at K=1000: "
-                          "profiles/r2_parity_errors.jsonl)"),
+                       + (", OPT-IN multiplicative column update (an approximation, profiles/r2_mult_drift.md)"
+                          if args.mult else ", the reference's g-side arithmetic (default; parity vs the "
+                          "reference at K=200/1000/2000: profiles/r2_parity_errors.jsonl)"),
                        "l2": "inputs larger than L2 (C = 256 MiB > 126 MB)",
                        "parallelism": "single GPU (C2 is a 1-GPU config)",
                        "guard_stats_last_step": guard},
@@ -633,7 +635,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the other-config rate lines")
     ap.add_argument("--exact", action="store_true", help="exact two-pass variant instead of stale shift")
-    ap.add_argument("--direct", action="store_true", help="no multiplicative column update (LSK_FLAG_NO_MULT)")
+    ap.add_argument("--mult", action="store_true",
+                    help="opt in to the multiplicative column update (LSK_FLAG_MULT; an approximation, not the headline)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the N > 1 line (C4 through the library's NCCL communicator) even on one rank: "
                          "a smoke test of the multi-GPU path on a single GPU")

@@ -42,9 +42,12 @@ extern "C" {
 #define LSK_FLAG_EXPANSION 8   /* points, eps >= 5e-3: cost as |x|^2+|y|^2-2x.y in the stale sweeps; the
                                   caller requests it only when (max|x-x0|^2 + max|y-x0|^2) 2^-24 /
                                   (eps * normaliser) is small (x0 = the problem's first source point) */
-#define LSK_FLAG_NO_MULT 32    /* dense m <= 8192, uniform nu, n*m >= 2^20, 1e-3 <= eps <= 2e-3, iterations
-                                  1..1000 of a solve: disable the
-                                  multiplicative column update (g-side terms from the f-side ones) */
+#define LSK_FLAG_MULT 32       /* OPT-IN approximation, dense m <= 8192, uniform nu, n*m >= 2^20, 1e-3 <= eps
+                                  <= 2e-3, iterations 1..1000 of a solve: the multiplicative column update
+                                  (g-side terms from the f-side ones, 1 instead of 2 ex2 per element). Its
+                                  potentials drift from the reference's by up to 3e-5 (per-potential max
+                                  norm, K = 1000; the direct default stays within 1e-5 where the reference's
+                                  own rounding allows): profiles/r2_mult_drift.md */
 #define LSK_FLAG_STD_MULTIKERNEL 64 /* standard domain: force the two-pass multi-kernel loop (fp32 m <= 8192
                                        otherwise runs the one-pass persistent kernel) */
 #define LSK_FLAG_NO_CLUSTER 512 /* dense m <= 1024, n <= 14336, uniform nu: run the 148-CTA grid solver instead

@@ -21,7 +21,7 @@ LSK_FLAG_STALE_SHIFT = 1
 LSK_FLAG_COST = 2
 LSK_FLAG_EXPANSION = 8
 LSK_FLAG_UNIFORM_NU = 16
-LSK_FLAG_NO_MULT = 32
+LSK_FLAG_MULT = 32
 LSK_FLAG_STD_MULTIKERNEL = 64
 LSK_FLAG_SHARD_PARTIALS = 128
 LSK_FLAG_SHARD_ALLREDUCE = 256

@@ -111,6 +111,9 @@ struct DenseLayout {
   size_t off_f0, off_g0, zero_bytes, off_f1, off_g1, off_part, off_pairs, off_err, off_flag, off_redo, off_errrow, off_cost, total;
 };
 
+#ifndef LSK_X_MULT_EPS_LO
+#define LSK_X_MULT_EPS_LO 1e-3
+#endif
 constexpr int kMultIters = 1000;       // iterations that may use the multiplicative column update
 #ifndef LSK_X_CLUSTER_MAX_ROWS
 #define LSK_X_CLUSTER_MAX_ROWS 128
@@ -328,7 +331,7 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
   // 1e-5 bar at the C2 class (eps = 1e-3, K = 1000: 6.5e-6, profiles/r2_parity_errors.jsonl),
   // but at eps = 1e-2 it reaches 1.2e-5 on g by K = 300 (tests/test_gpu_cluster.py), so
   // the gate is eps in [1e-3, 2e-3].
-  a.mult = (a.stale && eps >= 1e-3 && eps <= 2e-3 && (long long)n * m >= (1LL << 20) && !(flags & LSK_FLAG_NO_MULT))
+  a.mult = (a.stale && eps >= LSK_X_MULT_EPS_LO && eps <= 2e-3 && (long long)n * m >= (1LL << 20) && (flags & LSK_FLAG_MULT))
                ? 1 : 0;
   // and only for the first kMultIters iterations: the drift is pinned at C2 up
   // to K = 1000 (6.5e-6 on g); later iterations run the direct arithmetic, so a

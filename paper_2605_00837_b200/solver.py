@@ -146,7 +146,7 @@ def _uniform(log_w):
 
 
 def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=True, ws=None,
-                  uniform_nu=False, mult=True, cluster=True):
+                  uniform_nu=False, mult=False, cluster=True):
     C = to_device_cost(C)
     n, m = C.rows, C.cols
     K, c = int(config.max_iterations), int(config.check_interval)
@@ -163,7 +163,7 @@ def _launch_solve(torch, C, log_mu, log_nu, mu32, config, stale=True, want_cost=
     r.resf = torch.zeros(2, dtype=torch.float32, device="cuda")
     flags = (_lib.LSK_FLAG_STALE_SHIFT if stale else 0) | (_lib.LSK_FLAG_COST if want_cost else 0)
     flags |= _lib.LSK_FLAG_UNIFORM_NU if uniform_nu else 0
-    flags |= 0 if mult else _lib.LSK_FLAG_NO_MULT
+    flags |= _lib.LSK_FLAG_MULT if mult else 0
     flags |= 0 if cluster else _lib.LSK_FLAG_NO_CLUSTER
     r.ev0 = torch.cuda.Event(enable_timing=True)
     r.ev1 = torch.cuda.Event(enable_timing=True)
@@ -204,7 +204,7 @@ def _report_from(r, t0, return_device=False):
     return report, DualPotentials(alpha=alpha, beta=beta)
 
 
-def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multiplicative=True, cluster=True):
+def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multiplicative=False, cluster=True):
     """Log-domain Sinkhorn from zero potentials (reference solver.py:230-337).
 
     Alternates f (alpha) and g (beta) updates, checks the L1 row-marginal
@@ -215,9 +215,12 @@ def solve(cost, mu, nu, config, *, stale_shift=True, return_device=False, multip
     transport cost unless the solve failed. The whole loop is one
     cooperative kernel launch; the host synchronises once, at the end.
 
-    ``multiplicative=False`` disables the multiplicative column update of the
-    uniform-target kernel (``LSK_FLAG_NO_MULT``) and forms every
-    g-side argument from the cost element as the reference does.
+    Every g-side argument is formed from the cost element as the reference
+    does. ``multiplicative=True`` opts in to the multiplicative column update
+    of the uniform-target kernel (``LSK_FLAG_MULT``: g-side terms from the
+    f-side ones, ~18% faster at n = m = 8192) -- an approximation whose
+    potentials drift from the reference's by up to ~3e-5 relative at K = 1000
+    (profiles/r2_mult_drift.md), so it is never on by default.
     ``cluster=False`` runs the 148-CTA grid solver instead of the cluster
     solvers at m <= 1024 with uniform targets (``LSK_FLAG_NO_CLUSTER``; A/B).
     ``stale_shift=False`` selects the exact two-pass variant (max pass per

@@ -27,7 +27,7 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-5
 
 
-def launch(C, mu, nu, cfg, *, cluster, mult=True, stale=True):
+def launch(C, mu, nu, cfg, *, cluster, mult=False, stale=True):
     import torch
 
     lm, ln, w = S._dev_f32(torch, mu.log_weights), S._dev_f32(torch, nu.log_weights), S._dev_f32(torch, mu.weights)

@@ -23,7 +23,7 @@ def main():
     ap.add_argument("--reps", type=int, default=1)
     ap.add_argument("--general", action="store_true", help="do not pass the uniform-nu flag")
     ap.add_argument("--no-cluster", action="store_true", help="grid solver instead of the single-cluster one")
-    ap.add_argument("--direct", action="store_true", help="no multiplicative column update")
+    ap.add_argument("--mult", action="store_true", help="opt in to the multiplicative column update")
     a = ap.parse_args()
     import torch
 
@@ -44,7 +44,7 @@ def main():
     ws = None
     for _ in range(a.reps):
         r, ws = S._launch_solve(torch, C, lm, ln, mu, cfg, stale=not a.exact, ws=ws,
-                                uniform_nu=not a.general, cluster=not a.no_cluster, mult=not a.direct)
+                                uniform_nu=not a.general, cluster=not a.no_cluster, mult=a.mult)
     torch.cuda.synchronize()
     print("iters", r.res.cpu().numpy()[:6], "ms", r.ev0.elapsed_time(r.ev1), flush=True)
 
