@@ -50,7 +50,7 @@ extern "C" {
                                   own rounding allows): profiles/r2_mult_drift.md */
 #define LSK_FLAG_STD_MULTIKERNEL 64 /* standard domain: force the two-pass multi-kernel loop (fp32 m <= 8192
                                        otherwise runs the one-pass persistent kernel) */
-#define LSK_FLAG_NO_CLUSTER 512 /* dense m <= 1024, n <= 14336, uniform nu: run the 148-CTA grid solver instead
+#define LSK_FLAG_NO_CLUSTER 512 /* dense m <= 1024, n <= 30720, uniform nu: run the 148-CTA grid solver instead
                                    of the cluster solvers (single cluster n <= 128, multi-cluster above; A/B) */
 #define LSK_FLAG_UNIFORM_NU 16 /* dense m <= 8192: caller asserts log_nu[j] == log_nu[0] for all j (uniform
                                   target weights); the kernel verifies it and a violation ends the solve as

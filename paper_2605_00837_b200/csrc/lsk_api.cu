@@ -364,8 +364,11 @@ int32_t lsk_solve_dense_f32(const float* C, int64_t ldc, int32_t n, int32_t m, c
     lsk::DenseArgs ac = a;
     ac.mult = 0;  // the cluster solvers always run the reference's direct g-side arithmetic
     if (n > kClusterMaxRows) {
-#ifdef LSK_X_MC_CL8
-      if ((rc = launch_multicluster<8>(ac, L.G, st, done))) return rc;
+      // clusters of 8 first: up to 18 co-resident on a B200 (144 SMs) against 7 of 16 (112),
+      // so C1 gives every warp one row; 0.7-3.5% faster from 256 to 4096 rows
+      // (profiles/r2_c1_cluster.md)
+#ifndef LSK_X_MC_CL16
+      if (!done && (rc = launch_multicluster<8>(ac, L.G, st, done))) return rc;
 #endif
       if (!done && (rc = launch_multicluster<16>(ac, L.G, st, done))) return rc;
       if (!done && (rc = launch_multicluster<8>(ac, L.G, st, done))) return rc;

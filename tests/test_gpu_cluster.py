@@ -1,7 +1,7 @@
 """The cluster dense solvers (csrc/lsk_dense_cluster.cuh), uniform targets,
 m <= 1024: n <= 128 runs as ONE 16-CTA thread-block cluster with DSMEM
-exchanges; 128 < n <= 14336 as the multi-cluster solver (up to 7 clusters of
-16 CTAs on a B200, DSMEM inside a cluster, one software grid barrier per
+exchanges; 128 < n <= 30720 as the multi-cluster solver (up to 15 clusters of
+8 CTAs on a B200, DSMEM inside a cluster, one software grid barrier per
 iteration between them) -- both instead of the 148-CTA grid solver (the
 reference golden fixtures of those sizes in test_gpu_parity.py, C1 among
 them, also run through them).
