@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -100,7 +101,12 @@ extern "C" int32_t lsk_h2d_cost_f32(const void* src, int32_t src_is_f64, int64_t
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cfail("cudaGetDevice", e);
   const size_t row_bytes = size_t(ldd) * 4;
-  const int chunk_rows = int(std::max<size_t>(1, (size_t(4) << 20) / row_bytes));  // ~4 MB of fp32 per chunk
+  // ~1 MB of fp32 per chunk: C2's 8192 x 8192 fp64 matrix stages in 8.5 ms vs 9.0 ms with
+  // 4 MB and 12.3 ms with 16 MB chunks (tools/gpu_h2d.sh, 16 host cores; the pinned fp32
+  // PCIe floor is 4.9 ms). LSK_H2D_CHUNK_KB overrides it (experiments).
+  size_t chunk_bytes = size_t(1) << 20;
+  if (const char* v = getenv("LSK_H2D_CHUNK_KB")) chunk_bytes = std::max<size_t>(64, strtoull(v, nullptr, 10)) << 10;
+  const int chunk_rows = int(std::max<size_t>(1, chunk_bytes / row_bytes));
   const int nchunks = (n + chunk_rows - 1) / chunk_rows;
   int T = threads > 0 ? threads : int(std::thread::hardware_concurrency());
   T = std::max(1, std::min({T, nchunks, 32}));

@@ -17,7 +17,7 @@ n = 8192
 C = rng.uniform(0, 2, (n, n))
 out = torch.empty((n, n), dtype=torch.float32, device="cuda")
 print("cpus", os.cpu_count(), flush=True)
-for T in (0, 4, 8, 16, 24, 32):
+for T in [int(x) for x in os.environ.get("PROBE_T", "0 4 8 16 24 32").split()]:
     ts = []
     for _ in range(4):
         torch.cuda.synchronize()
