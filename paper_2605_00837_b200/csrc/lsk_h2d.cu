@@ -14,6 +14,7 @@
 // CPU (cvtsd2ss, round-to-nearest-even, subnormals kept) is bit-identical to
 // __double2float_rn.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <atomic>
@@ -31,6 +32,20 @@ int32_t fail(int32_t code, const std::string& msg);
 }
 
 namespace {
+
+// one row fp64 -> fp32 (round-to-nearest-even, as cvtsd2ss): 16-byte
+// non-temporal stores into the pinned chunk (no read-for-ownership of the
+// destination lines: ~1/4 less host memory traffic per call; the DMA reads the
+// chunk after the worker's sfence). o must be 16-byte aligned.
+void row_f64_to_f32_nt(const double* in, float* o, int m) {
+  int j = 0;
+  for (; j + 4 <= m; j += 4) {
+    const __m128 lo = _mm_cvtpd_ps(_mm_loadu_pd(in + j));
+    const __m128 hi = _mm_cvtpd_ps(_mm_loadu_pd(in + j + 2));
+    _mm_stream_ps(o + j, _mm_movelh_ps(lo, hi));
+  }
+  for (; j < m; ++j) o[j] = static_cast<float>(in[j]);
+}
 
 struct Worker {
   cudaStream_t s = nullptr;
@@ -103,7 +118,8 @@ extern "C" int32_t lsk_h2d_cost_f32(const void* src, int32_t src_is_f64, int64_t
   const size_t row_bytes = size_t(ldd) * 4;
   // ~1 MB of fp32 per chunk: C2's 8192 x 8192 fp64 matrix stages in 8.5 ms vs 9.0 ms with
   // 4 MB and 12.3 ms with 16 MB chunks (tools/gpu_h2d.sh, 16 host cores; the pinned fp32
-  // PCIe floor is 4.9 ms). LSK_H2D_CHUNK_KB overrides it (experiments).
+  // PCIe floor is 4.9 ms on that box); with the non-temporal stores 7.4 vs 8.2 ms on a box
+  // whose floor is 6.05 ms. LSK_H2D_CHUNK_KB overrides it (experiments).
   size_t chunk_bytes = size_t(1) << 20;
   if (const char* v = getenv("LSK_H2D_CHUNK_KB")) chunk_bytes = std::max<size_t>(64, strtoull(v, nullptr, 10)) << 10;
   const int chunk_rows = int(std::max<size_t>(1, chunk_bytes / row_bytes));
@@ -120,6 +136,9 @@ extern "C" int32_t lsk_h2d_cost_f32(const void* src, int32_t src_is_f64, int64_t
   if (e != cudaSuccess) return cfail("cudaEventCreate", e);
   cudaEventRecord(start, st);
   for (int t = 0; t < T; ++t) cudaStreamWaitEvent(p.w[t].s, start, 0);
+  // rows are 16-byte aligned in the pinned chunk when ldd % 4 == 0 (cudaHostAlloc is page aligned)
+  const char* ntenv = getenv("LSK_H2D_NT");
+  const bool nt = ldd % 4 == 0 && !(ntenv && ntenv[0] == '0');
   std::atomic<int> err{0};
   std::string err_msg;
   auto body = [&](int t) {
@@ -133,12 +152,15 @@ extern "C" int32_t lsk_h2d_cost_f32(const void* src, int32_t src_is_f64, int64_t
         float* o = out + size_t(r - r0) * ldd;
         if (src_is_f64) {
           const double* in = static_cast<const double*>(src) + size_t(r) * lds;
-          for (int j = 0; j < m; ++j) o[j] = static_cast<float>(in[j]);
+          if (nt) row_f64_to_f32_nt(in, o, m);
+          else
+            for (int j = 0; j < m; ++j) o[j] = static_cast<float>(in[j]);
         } else {
           std::memcpy(o, static_cast<const float*>(src) + size_t(r) * lds, size_t(m) * 4);
         }
         for (int64_t j = m; j < ldd; ++j) o[j] = 0.f;
       }
+      if (nt) _mm_sfence();
       cudaError_t ce = cudaMemcpyAsync(dst + size_t(r0) * ldd, out, size_t(r1 - r0) * row_bytes,
                                        cudaMemcpyHostToDevice, w.s);
       if (ce == cudaSuccess) ce = cudaEventRecord(w.ev[k], w.s);
