@@ -152,7 +152,10 @@ int32_t lsk_build_cost_f32(const double* X, const double* Y, int32_t n, int32_t 
  * the host: `threads` workers (0 = all cores) each round a row chunk into their
  * own pinned buffer and copy it asynchronously while rounding the next; the
  * copies are ordered before later work on `stream`. Replaces the pageable
- * cudaMemcpy + device cast of CostMatrix.values (types.py:60-86). */
+ * cudaMemcpy + device cast of CostMatrix.values (types.py:60-86). Chunks are
+ * ~1 MB of fp32 written with non-temporal stores when ldd % 4 == 0; the
+ * rounding is bit-identical either way (LSK_H2D_NT=0 / LSK_H2D_CHUNK_KB=<kb>
+ * in the environment override both, for experiments). */
 int32_t lsk_h2d_cost_f32(const void* src, int32_t src_is_f64, int64_t lds, int32_t n, int32_t m, float* dst,
                          int64_t ldd, int32_t threads, void* stream);
 
